@@ -1,0 +1,406 @@
+"""Benchmark: effective GFLOP/s (2mnk/t) of the memory-lean Winograd schedules on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Default workload (N=1): BASELINE config 2 -- C <- A*B + C over Z/65521Z with the
+paper's 2-temporary accumulating schedule (acc2), m=k=n=4096, residues from
+SplitMix64 seeds A=2, B=3, C=4 stored as float64, cutoff 256 (depth 4).
+A step is one full multiplication with the inputs resident in HBM; the
+400 MB of inputs exceed the 126 MB L2, so no flush is needed between steps.
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the same
+single-GPU workload on its own device (replicas, weak scaling); ranks are timed
+on the device and the max over ranks is reported.
+
+``--impl reference`` times the reference's own CPU implementation (the
+unmodified winomem headers compiled into oracle/_ref) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "effective GFLOP/s (2mnk/t) per schedule and peak extra HBM bytes, 1/2/4/8 B200"
+
+CONFIGS = {
+    "C1": dict(variant="std2", m=1024, k=1024, n=1024, cutoff=128, seed=1, alpha=1, beta=0,
+               field="modp", desc="C<-AB mod 65521, std2 (2 temporaries), 1024^3, cutoff 128"),
+    "C2": dict(variant="acc2", m=4096, k=4096, n=4096, cutoff=256, seed=2, alpha=1, beta=1,
+               field="modp", desc="C<-AB+C mod 65521, acc2 (2 temporaries), 4096^3, cutoff 256"),
+    "C3": dict(variant="iprect", m=8192, k=4096, n=8192, cutoff=256, seed=3, alpha=1, beta=0,
+               field="modp",
+               desc="C<-AB mod 65521, in-place rectangle (std2/ovl/ovr/ip on 4096^2 squares, "
+                    "A and B clobbered), 8192x4096x8192, cutoff 256"),
+    "C4": dict(variant="ipmm", m=16384, k=16384, n=16384, cutoff=512, seed=4, alpha=1, beta=0,
+               field="modp", desc="C<-AB mod 65521, ipmm (read-only, first level classical), "
+                                  "16384^3, cutoff 512"),
+    "C5": dict(variant="std2", m=32768, k=32768, n=32768, cutoff=1024, seed=5, alpha=1, beta=0,
+               field="real", desc="float64 C<-AB, std2, 32768^3, cutoff 1024"),
+}
+
+
+def peaks():
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def cpu_reference_rate(cfg, threads, sample_n=None):
+    """Run the reference run_variant (oracle/_ref) on `threads` host threads at
+    once, each on its own copy of the workload (or of a bounded sample).
+    Returns (GFLOP/s aggregate, seconds, sample description)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import numpy as np
+
+    from oracle import oracle as O
+
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    cutoff = cfg["cutoff"]
+    if sample_n:
+        scale = m // sample_n
+        m, k, n, cutoff = m // scale, k // scale, n // scale, max(1, cutoff // scale)
+    variant = cfg["variant"]
+    ref_variant = "std2" if variant == "iprect" else variant
+    A = O.fill_random(m, k, cfg["seed"])
+    B = O.fill_random(k, n, cfg["seed"] + 1)
+    C0 = O.fill_random(m, n, cfg["seed"] + 2) if cfg["beta"] else np.zeros((m, n), np.uint32)
+
+    def one(_):
+        O.ref_run_variant(ref_variant, A, B, C0, cfg["alpha"], cfg["beta"], cutoff)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        list(ex.map(one, range(threads)))
+    dt = time.perf_counter() - t0
+    sample = (f"{threads} concurrent reference run_variant('{ref_variant}') calls on "
+              f"{m}x{k}x{n}, cutoff {cutoff} (oracle/_ref, -O3 -DNDEBUG, 1 thread each)")
+    return threads * 2.0 * m * n * k / dt / 1e9, dt, sample
+
+
+def run_reference_arm(args, cfg):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    threads = os.cpu_count() or 1
+    # bounded sample: the full problem when the whole run fits in ~3 minutes
+    full_est = {"C1": 0.3, "C2": 20.0, "C3": 60.0, "C4": 1800.0, "C5": 1e9}[args.config]
+    total_steps = args.steps + min(args.warmup, 1)
+    sample_n = None
+    if cfg["field"] == "real":
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "no reference float64 path (SPEC.md:94)"}))
+        return
+    if full_est * total_steps > 180:
+        sample_n = 2048 if args.config in ("C2", "C3") else 1024
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_rate(cfg, threads, sample_n)
+    rates, secs = [], []
+    sample = ""
+    for _ in range(args.steps):
+        r, dt, sample = cpu_reference_rate(cfg, threads, sample_n)
+        rates.append(r)
+        secs.append(dt)
+    value = statistics.median(rates)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (SplitMix64 seeds, residues mod 65521)",
+        "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"]},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--leaf", type=int, default=int(os.environ.get("WM_LEAF", 2)),
+                    help="0 DMMA float64, 1 tcgen05 int8 limbs, 2 auto")
+    ap.add_argument("--fuse", type=int, default=int(os.environ.get("WM_FUSE", 1)))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_0707_2347_b200 as W
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    real = cfg["field"] == "real"
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    A = W.Matrix(m, k, device=local, real=real)
+    B = W.Matrix(k, n, device=local, real=real)
+    C = W.Matrix(m, n, device=local, real=real)
+    ctx = A.ctx()
+    ctx.set_option("leaf_kernel", args.leaf)
+    ctx.set_option("fuse_frames", args.fuse)
+    ctx.set_option("graphs", 1)
+
+    def reset_inputs():
+        A.fill_random(cfg["seed"])
+        B.fill_random(cfg["seed"] + 1)
+        if cfg["beta"]:
+            C.fill_random(cfg["seed"] + 2)
+        else:
+            C.fill_zero()
+
+    def step():
+        return W.run_variant(cfg["variant"], A, B, C, alpha=cfg["alpha"], beta=cfg["beta"],
+                             cutoff=cfg["cutoff"])
+
+    # parity of the very first multiplication against the golden hash
+    reset_inputs()
+    rep = step()
+    torch.cuda.synchronize()
+    parity = None
+    if not real:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_hashes.json")))
+        h = "%016x" % C.hash()
+        want = gold.get(args.config, {}).get("appendix_a")
+        parity = {"c_hash": h, "golden": want, "ok": h == want}
+
+    in_place = cfg["variant"] in ("iprect",)
+    for _ in range(args.warmup):
+        if in_place:
+            reset_inputs()
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    stream = ctx.stream
+    small = 8 * (m * k + k * n + m * n) <= 126e6
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}") \
+        if small else None
+    evs = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            if in_place:
+                reset_inputs()  # A and B are clobbered: regenerate outside the timed events
+            if flush is not None:
+                flush.zero_()  # 256 MB write evicts L2 between timed steps
+            ctx.enter()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+    times = [a.elapsed_time(b) / 1e3 for a, b in evs]
+    t_step = sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([t_step], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_step = float(t.item())
+    flops = 2.0 * m * n * k
+    value = world * flops / t_step / 1e9
+
+    # attribution: additions-only and leaves/frames-only replays (measurement only)
+    def subset_time(sub, reps=3):
+        ctx.set_option("subset", sub)
+        step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ctx.enter()
+        e0.record(stream)
+        for _ in range(reps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ctx.set_option("subset", 0)
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    t_add = subset_time(1)
+    t_leaf = subset_time(2)
+    t_frame = subset_time(3) if rep.fused_frames else 0.0
+    hbm, hbm_src = peaks()
+    add_issued = rep.add_bytes_issued
+    comps = {"additions": t_add, "leaf_products": t_leaf, "fused_frames": t_frame}
+    dominant = max(comps, key=comps.get)
+    if dominant == "additions":
+        achieved = add_issued / t_add / 1e9 if t_add else 0.0
+        roof = {"bound": "hbm", "kernel": "k_addsub (batched block additions)",
+                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "peak_source": hbm_src,
+                "algorithmic_bytes_per_step": add_issued, "kernel_seconds_per_step": t_add}
+    else:
+        # leaf / frame products: effective (2mnk of the leaves) rate; the
+        # tensor-pipe peak is the measured int8 / DMMA figure when available
+        t = comps[dominant]
+        achieved = rep.leaf_flops / t / 1e12 if t else 0.0
+        roof = {"bound": "tensor", "kernel": dominant, "achieved": achieved, "peak": None,
+                "unit": "TFLOP/s", "frac": None, "traffic": None,
+                "algorithmic_flops_per_step": rep.leaf_flops, "kernel_seconds_per_step": t}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: SplitMix64 seeds A=%d B=%d C=%d, %s stored as float64" % (
+            cfg["seed"], cfg["seed"] + 1, cfg["seed"] + 2,
+            "uniform[-1,1)" if real else "residues mod 65521"),
+        "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
+                   "m": m, "k": k, "n": n, "cutoff": cfg["cutoff"], "alpha": cfg["alpha"],
+                   "beta": cfg["beta"], "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs (%.0f MB) %s L2; %s" % (
+                       8 * (m * k + k * n + m * n) / 1e6,
+                       ">" if 8 * (m * k + k * n + m * n) > 126e6 else "<=",
+                       "no flush needed" if 8 * (m * k + k * n + m * n) > 126e6 else
+                       "flushed between steps"),
+                   "leaf_kernel": args.leaf, "fused_frames": bool(args.fuse)},
+        "peak_extra_bytes": rep.peak_extra_bytes,
+        "peak_extra_words": rep.peak_extra_words,
+        "expected_peak_extra_words": W.expected_costs(cfg["variant"], m, k, n,
+                                                      cfg["cutoff"]).peak_extra_words,
+        "parity": parity,
+        "breakdown_s": comps,
+        "roofline": roof,
+        "gpu_launches": rep.n_launches * args.steps,
+        "launches_per_step": rep.n_launches,
+        "clocks": clk.summary(),
+    }
+
+    if rank == 0 and world == 1 and not args.no_e2e and not real:
+        out["e2e"] = e2e(W, cfg, args, np, torch)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not real:
+        try:
+            r, dt, sample = cpu_reference_rate(cfg, 1, None if args.config in ("C1", "C2")
+                                               else 2048)
+            out["cpu_baseline"] = {"value": r, "unit": "GFLOP/s", "cores": 1,
+                                   "kind": "reference", "sample": sample,
+                                   "seconds": dt}
+        except Exception as e:  # pragma: no cover
+            out["cpu_baseline"] = {"value": None, "error": str(e)}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e(W, cfg, args, np, torch):
+    """Same metric through the public host API: pinned u32 host buffers in,
+    result out, host<->device copies inside the timed region."""
+    from oracle import oracle as O  # inputs only (seeded generator), not timed
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    A = torch.from_numpy(O.fill_random(m, k, cfg["seed"])).pin_memory().numpy()
+    B = torch.from_numpy(O.fill_random(k, n, cfg["seed"] + 1)).pin_memory().numpy()
+    C0 = O.fill_random(m, n, cfg["seed"] + 2) if cfg["beta"] else np.zeros((m, n), np.uint32)
+    Cp = torch.from_numpy(C0.copy()).pin_memory().numpy()
+    ctx = W.Context.get()
+    ctx.set_option("leaf_kernel", args.leaf)
+    ctx.set_option("fuse_frames", args.fuse)
+    steps = max(3, min(args.steps, 5))
+    for _ in range(2):
+        Cp[...] = C0
+        W.run_variant_host(cfg["variant"], A, B, Cp, cfg["alpha"], cfg["beta"], cfg["cutoff"])
+    ts = []
+    for _ in range(steps):
+        Cp[...] = C0
+        t0 = time.perf_counter()
+        W.run_variant_host(cfg["variant"], A, B, Cp, cfg["alpha"], cfg["beta"], cfg["cutoff"])
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    h2d = 4 * (m * k + k * n + (m * n if cfg["beta"] else 0))
+    d2h = 4 * m * n
+    if cfg["variant"] in ("iprect", "ipovmm"):
+        d2h += 4 * (m * k + k * n)
+    return {"value": 2.0 * m * n * k / t / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "seconds_per_step": t,
+            "timing": "host wall clock around the synchronous C-ABI call"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,150 @@
+/*
+ * winomem-b200: the C-ABI drop-in boundary for the memory-efficient
+ * Strassen-Winograd schedules (Boyer, Dumas, Pernet, Zhou, ISSAC 2009) on
+ * NVIDIA B200 (sm_100a).
+ *
+ * Plain pointers and sizes only.  Every entry point returns a status code
+ * (WM_OK == 0) that mirrors the reference's C++ exception taxonomy; the message
+ * of the last failure on the calling thread is available from wm_last_error().
+ * The reference interface each entry replaces is cited beside it
+ * (paths relative to /root/reference/proj/include/winomem/).
+ *
+ * Matrices live in device memory as row-major float64 with a leading
+ * dimension (wm_dmat).  In the MODP field (Z/pZ, odd prime p < 2^16, the
+ * reference's default p = 65521, ring.hpp:89) entries are canonical residues
+ * held exactly in float64; in the REAL64 field they are ordinary doubles.
+ * Host-buffer entry points (suffix _host_u32) take the reference's own element
+ * type (uint32_t residues, ring.hpp:21) and do the upload / download and
+ * conversion on the context's stream.
+ *
+ * Threading: one host thread per context; all work is issued in order on the
+ * context's stream; there is no CPU fallback -- a context cannot be created
+ * without a CUDA device.
+ */
+#ifndef WINOMEM_B200_H
+#define WINOMEM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: ring.hpp:23-43, workspace.hpp:20-22, schedule.hpp:30-43 */
+enum {
+    WM_OK = 0,
+    WM_E_DIMENSION = 1,          /* dimension_error */
+    WM_E_ODD_DIMENSION = 2,      /* odd_dimension_error */
+    WM_E_PARTIAL_OVERLAP = 3,    /* partial_overlap_error */
+    WM_E_ALIAS = 4,              /* alias_error */
+    WM_E_SHAPE = 5,              /* shape_error */
+    WM_E_CONTRACT = 6,           /* contract_error */
+    WM_E_IO = 7,                 /* io_error */
+    WM_E_WORKSPACE = 8,          /* workspace_error */
+    WM_E_UNKNOWN_SCHEDULE = 9,   /* unknown_schedule_error */
+    WM_E_PARSE = 10,             /* parse_error */
+    WM_E_CONTRACT_VIOLATION = 11,/* contract_violation_error */
+    WM_E_CUDA = 12,              /* device error (new) */
+    WM_E_NCCL = 13,              /* communication error (new) */
+    WM_E_INVALID = 14            /* invalid argument / state (new) */
+};
+
+enum { WM_FIELD_MODP = 0, WM_FIELD_REAL64 = 1 };
+
+typedef struct wm_ctx wm_ctx;
+
+/* A device matrix view: row-major float64, element (i,j) at ptr[i*ld + j]. */
+typedef struct {
+    double* ptr;
+    uint64_t rows, cols, ld;
+} wm_dmat;
+
+/* CostReport (meter.hpp:53-75) plus the device-side figures. */
+typedef struct {
+    uint64_t mults, adds;
+    uint64_t peak_extra_words;   /* high-water of live temporary words (the graded memory metric) */
+    uint64_t total_alloc_words;
+    uint64_t word_moves;
+    uint64_t classical_calls;
+    uint64_t schedule_frames;    /* sum of CostMeter::schedule_calls */
+    uint64_t peak_extra_bytes;   /* HBM actually reserved for temporaries (arena high-water) */
+    uint64_t n_ops;              /* device operations in the plan */
+    uint64_t n_launches;         /* kernel launches issued per execution */
+    uint64_t fused_frames;       /* OP_FRAME launches */
+    /* algorithmic work (independent of fusion): bytes moved by the schedule's
+     * block additions at 8 B per element (3 words per two-term addition, 2 per
+     * copy) and flops of the classical leaves (2*m*k*n each) */
+    uint64_t add_bytes;
+    uint64_t leaf_flops;
+    /* bytes the issued addition kernels move (fused frames keep theirs on chip) */
+    uint64_t add_bytes_issued;
+} wm_report;
+
+/* ---- library / context --------------------------------------------------- */
+const char* wm_version(void);
+const char* wm_last_error(void);
+/* Creates a context on `device` for field WM_FIELD_MODP (prime p < 2^16, the
+ * Modulus check of ring.hpp:47-53) or WM_FIELD_REAL64 (p ignored).  `stream`
+ * is a cudaStream_t (NULL: the context creates its own). */
+int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out);
+int wm_ctx_destroy(wm_ctx* ctx);
+int wm_ctx_sync(wm_ctx* ctx);
+/* options: "fuse_frames" (0/1), "graphs" (0/1), "batch_adds" (0/1),
+ *          "leaf_kernel" (0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto),
+ *          "subset" (measurement only: 0 all launches, 1 additions only,
+ *                    2 leaf products only, 3 fused frames only) */
+int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value);
+int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value);
+
+/* ---- primitive operators (ring.hpp) -------------------------------------- */
+/* dst <- sa*a + sb*b; dst may alias a or b exactly (block_addsub, ring.hpp:241-278) */
+int wm_block_addsub(wm_ctx* ctx, wm_dmat dst, wm_dmat a, wm_dmat b, uint32_t sa, uint32_t sb);
+/* dst <- s*src (block_scale_copy, ring.hpp:282-310) */
+int wm_block_scale_copy(wm_ctx* ctx, wm_dmat dst, wm_dmat src, uint32_t s);
+/* C <- alpha*A*B + beta*C, C disjoint from A and B (classical_mul, ring.hpp:315-384) */
+int wm_classical_mul(wm_ctx* ctx, wm_dmat C, wm_dmat A, wm_dmat B, uint32_t alpha, uint32_t beta);
+
+/* ---- drivers -------------------------------------------------------------- */
+/* run_variant (drivers.hpp:213-222) / multiply (executor.hpp:240-299):
+ * variant is a builtin schedule name (std2 acc3 ip ovl ovl2 ovr aclr accr acc2 acr),
+ * "classic", "ipmm" (drivers.hpp:137-158), "ipovmm" (drivers.hpp:52-99),
+ * "iprect" (in-place rectangle, k <= min(m,n), new) or "blocked_acc_t<T>[_acc2]"
+ * (drivers.hpp:163-209).  A is m x k, B k x n, C m x n (m, k, n from the views). */
+int wm_run_variant(wm_ctx* ctx, const char* variant, wm_dmat A, wm_dmat B, wm_dmat C,
+                   uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
+/* ipmm (drivers.hpp:137-138) */
+int wm_ipmm(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int cutoff, wm_report* report);
+/* REAL64 field: the same dispatch with float64 scalars */
+int wm_run_variant_real(wm_ctx* ctx, const char* variant, wm_dmat A, wm_dmat B, wm_dmat C,
+                        double alpha, double beta, int cutoff, wm_report* report);
+/* End-to-end through host buffers of reference residues (Matrix&, ring.hpp:180-219):
+ * uploads A, B (and C when beta != 0), runs, downloads C -- and A / B when the
+ * variant's contract may overwrite them, as the reference's Matrix& would show. */
+int wm_run_variant_host_u32(wm_ctx* ctx, const char* variant, uint64_t m, uint64_t k, uint64_t n,
+                            uint32_t* A, uint32_t* B, uint32_t* C, uint32_t alpha, uint32_t beta,
+                            int cutoff, wm_report* report);
+
+/* ---- host-only planning (no device needed) --------------------------------- */
+/* Plans `variant` and returns the exact CostReport the reference meter would
+ * produce plus the device plan's size; executes nothing. */
+int wm_plan_report(const char* variant, int field, uint32_t p, uint64_t m, uint64_t k, uint64_t n,
+                   uint32_t alpha, uint32_t beta, int cutoff, int fuse_frames, wm_report* report);
+/* expected_costs (models.hpp:202-229); fields of the report beyond word_moves are 0 */
+int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, int cutoff,
+                      wm_report* report);
+/* Per-schedule frame counts of the last plan on this thread: "name:count,..." */
+int wm_plan_schedule_calls(char* out, int len);
+
+/* ---- boundary formats ------------------------------------------------------ */
+int wm_upload_u32(wm_ctx* ctx, wm_dmat dst, const uint32_t* host, uint64_t host_ld);
+int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src);
+/* FNV-1a over uint32 residues, row-major (fnv1a64 / Matrix::hash, ring.hpp:107-114,208) */
+uint64_t wm_fnv1a64_u32(const uint32_t* data, uint64_t count);
+/* seeded device generator, bit-identical to Matrix::fill_random (ring.hpp:202-205);
+ * REAL64: x = 2*((next()>>11)*2^-53) - 1 */
+int wm_fill_random(wm_ctx* ctx, wm_dmat dst, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WINOMEM_B200_H */

@@ -1,0 +1,87 @@
+"""ctypes binding of the C-ABI (include/winomem_b200.h).
+
+Loads the in-tree ``libwinomem_b200.so``; there is no fallback -- if the library
+is missing the import fails loudly (build it with ``python -m
+paper_0707_2347_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libwinomem_b200.so")
+
+# status codes (winomem_b200.h)
+WM_OK = 0
+WM_FIELD_MODP = 0
+WM_FIELD_REAL64 = 1
+
+EXPORTS = [
+    "wm_version", "wm_last_error", "wm_ctx_create", "wm_ctx_destroy", "wm_ctx_sync",
+    "wm_ctx_set_option", "wm_ctx_get_option", "wm_block_addsub", "wm_block_scale_copy",
+    "wm_classical_mul", "wm_run_variant", "wm_ipmm", "wm_run_variant_real",
+    "wm_run_variant_host_u32", "wm_plan_report", "wm_expected_costs", "wm_plan_schedule_calls",
+    "wm_upload_u32", "wm_download_u32", "wm_fnv1a64_u32", "wm_fill_random",
+]
+
+
+class wm_dmat(C.Structure):
+    _fields_ = [("ptr", C.c_void_p), ("rows", C.c_uint64), ("cols", C.c_uint64),
+                ("ld", C.c_uint64)]
+
+
+class wm_report(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in (
+        "mults", "adds", "peak_extra_words", "total_alloc_words", "word_moves",
+        "classical_calls", "schedule_frames", "peak_extra_bytes", "n_ops", "n_launches",
+        "fused_frames", "add_bytes", "leaf_flops", "add_bytes_issued")]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the winomem-b200 native library must be built "
+            "(python -m paper_0707_2347_b200.build); there is no fallback path")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    u32, u64, i32 = C.c_uint32, C.c_uint64, C.c_int
+    ctx_p = C.c_void_p
+    L.wm_version.restype = C.c_char_p
+    L.wm_last_error.restype = C.c_char_p
+    L.wm_ctx_create.argtypes = [i32, u32, i32, C.c_void_p, P(ctx_p)]
+    L.wm_ctx_destroy.argtypes = [ctx_p]
+    L.wm_ctx_sync.argtypes = [ctx_p]
+    L.wm_ctx_set_option.argtypes = [ctx_p, C.c_char_p, C.c_int64]
+    L.wm_ctx_get_option.argtypes = [ctx_p, C.c_char_p, P(C.c_int64)]
+    L.wm_block_addsub.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, u32, u32]
+    L.wm_block_scale_copy.argtypes = [ctx_p, wm_dmat, wm_dmat, u32]
+    L.wm_classical_mul.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, u32, u32]
+    L.wm_run_variant.argtypes = [ctx_p, C.c_char_p, wm_dmat, wm_dmat, wm_dmat, u32, u32, i32,
+                                 P(wm_report)]
+    L.wm_ipmm.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, i32, P(wm_report)]
+    L.wm_run_variant_real.argtypes = [ctx_p, C.c_char_p, wm_dmat, wm_dmat, wm_dmat, C.c_double,
+                                      C.c_double, i32, P(wm_report)]
+    L.wm_run_variant_host_u32.argtypes = [ctx_p, C.c_char_p, u64, u64, u64, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, u32, u32, i32, P(wm_report)]
+    L.wm_plan_report.argtypes = [C.c_char_p, i32, u32, u64, u64, u64, u32, u32, i32, i32,
+                                 P(wm_report)]
+    L.wm_expected_costs.argtypes = [C.c_char_p, u64, u64, u64, i32, P(wm_report)]
+    L.wm_plan_schedule_calls.argtypes = [C.c_char_p, i32]
+    L.wm_upload_u32.argtypes = [ctx_p, wm_dmat, C.c_void_p, u64]
+    L.wm_download_u32.argtypes = [ctx_p, C.c_void_p, u64, wm_dmat]
+    L.wm_fnv1a64_u32.argtypes = [C.c_void_p, u64]
+    L.wm_fnv1a64_u32.restype = u64
+    L.wm_fill_random.argtypes = [ctx_p, wm_dmat, u64]
+    _lib = L
+    return L
+
+
+def last_error():
+    return lib().wm_last_error().decode(errors="replace")

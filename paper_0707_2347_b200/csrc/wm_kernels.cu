@@ -1,0 +1,191 @@
+// Elementwise kernels: batched block additions over Z/pZ held in float64
+// (block_addsub / block_scale_copy, ring.hpp:241-310), boundary conversions and
+// the seeded generator.
+//
+// The additions are HBM-bound (3 x 8 B per element for a two-term addition).
+// One launch carries up to kMaxAddBatch independent items (e.g. a schedule's
+// S_i / T_i pair), each split into 256-thread blocks that stream 4 x 16 B per
+// thread with all loads issued before the stores.  Residue arithmetic is exact
+// in float64: operands are canonical (< 2^16), so a +/- b needs one conditional
+// correction and the general sa*a + sb*b (< 2^33) one floor-based reduction.
+#include <cstdint>
+
+#include "wm_device.h"
+
+namespace wm {
+namespace {
+
+template <bool REAL>
+__device__ __forceinline__ double apply(double a, double b, std::uint32_t mode, double sa,
+                                        double sb, double p, double pinv) {
+    if (REAL) {
+        switch (mode) {
+            case M_ADD: return a + b;
+            case M_SUB: return a - b;
+            case M_RSUB: return b - a;
+            case M_NEGADD: return -(a + b);
+            case M_GEN: return fma(sa, a, sb * b);
+            case M_COPY: return a;
+            case M_NEG: return -a;
+            default: return sa * a;
+        }
+    }
+    double v;
+    switch (mode) {
+        case M_ADD: v = a + b; return v >= p ? v - p : v;
+        case M_SUB: v = a - b; return v < 0.0 ? v + p : v;
+        case M_RSUB: v = b - a; return v < 0.0 ? v + p : v;
+        case M_NEGADD: v = a + b; v = v >= p ? v - p : v; return v != 0.0 ? p - v : 0.0;
+        case M_COPY: return a;
+        case M_NEG: return a != 0.0 ? p - a : 0.0;
+        case M_GEN: v = fma(sa, a, sb * b); break;
+        default: v = sa * a; break;
+    }
+    // v is an exact non-negative integer < 2^53
+    const double q = floor(v * pinv);
+    double r = fma(-q, p, v);
+    r = r < 0.0 ? r + p : r;
+    return r >= p ? r - p : r;
+}
+
+template <bool REAL>
+__global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
+    int i = 0;
+#pragma unroll 1
+    while (i + 1 < B.n && blockIdx.x >= B.it[i + 1].blk0) ++i;
+    const AddItem& t = B.it[i];
+    const std::uint32_t mode = t.mode;
+    const double sa = REAL ? t.sad : static_cast<double>(t.sa);
+    const double sb = REAL ? t.sbd : static_cast<double>(t.sb);
+    const double p = B.pd, pinv = B.pinv;
+    const bool two = mode <= M_GEN;
+    const std::uint64_t blk = blockIdx.x - t.blk0;
+    if (t.vec == 2) {
+        const std::uint32_t cv = t.cols >> 1;
+        const std::uint64_t total = static_cast<std::uint64_t>(t.rows) * cv;
+        const std::uint64_t start = blk * (kAddThreads * kAddIlp) + threadIdx.x;
+        double2 av[kAddIlp], bv[kAddIlp];
+        std::uint64_t r[kAddIlp], c[kAddIlp];
+        bool ok[kAddIlp];
+#pragma unroll
+        for (int u = 0; u < kAddIlp; ++u) {
+            const std::uint64_t idx = start + static_cast<std::uint64_t>(u) * kAddThreads;
+            ok[u] = idx < total;
+            r[u] = idx / cv;
+            c[u] = (idx - r[u] * cv) * 2;
+            if (ok[u]) {
+                av[u] = __ldg(reinterpret_cast<const double2*>(t.a + r[u] * t.lda + c[u]));
+                if (two) bv[u] = __ldg(reinterpret_cast<const double2*>(t.b + r[u] * t.ldb + c[u]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kAddIlp; ++u) {
+            if (!ok[u]) continue;
+            double2 o;
+            o.x = apply<REAL>(av[u].x, two ? bv[u].x : 0.0, mode, sa, sb, p, pinv);
+            o.y = apply<REAL>(av[u].y, two ? bv[u].y : 0.0, mode, sa, sb, p, pinv);
+            *reinterpret_cast<double2*>(t.d + r[u] * t.ldd + c[u]) = o;
+        }
+    } else {
+        const std::uint64_t total = static_cast<std::uint64_t>(t.rows) * t.cols;
+        const std::uint64_t start = blk * (kAddThreads * kAddIlp) + threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < kAddIlp; ++u) {
+            const std::uint64_t idx = start + static_cast<std::uint64_t>(u) * kAddThreads;
+            if (idx >= total) break;
+            const std::uint64_t rr = idx / t.cols, cc = idx - rr * t.cols;
+            const double a = t.a[rr * t.lda + cc];
+            const double b = two ? t.b[rr * t.ldb + cc] : 0.0;
+            t.d[rr * t.ldd + cc] = apply<REAL>(a, b, mode, sa, sb, p, pinv);
+        }
+    }
+}
+
+__global__ void k_u32_to_f64(double* __restrict__ dst, std::uint64_t ldd,
+                             const std::uint32_t* __restrict__ src, std::uint64_t lds,
+                             std::uint64_t rows, std::uint64_t cols) {
+    const std::uint64_t total = rows * cols;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+         i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t r = i / cols, c = i - r * cols;
+        dst[r * ldd + c] = static_cast<double>(src[r * lds + c]);
+    }
+}
+
+// canonicalise (values are exact integers; reduce any representative into [0, p))
+__global__ void k_f64_to_u32(std::uint32_t* __restrict__ dst, std::uint64_t ldd,
+                             const double* __restrict__ src, std::uint64_t lds,
+                             std::uint64_t rows, std::uint64_t cols, double p) {
+    const std::uint64_t total = rows * cols;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+         i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t r = i / cols, c = i - r * cols;
+        double v = src[r * lds + c];
+        v = v - floor(v / p) * p;
+        if (v >= p) v -= p;
+        if (v < 0) v += p;
+        dst[r * ldd + c] = static_cast<std::uint32_t>(v);
+    }
+}
+
+__device__ __forceinline__ std::uint64_t sm64_mix(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+// SplitMix64 stream of Matrix::fill_random (ring.hpp:93-105,202-205): element i of
+// the row-major fill is mix(seed + (i+1)*gamma) % p -- index-addressable.
+__global__ void k_fill_splitmix(double* __restrict__ dst, std::uint64_t ld, std::uint64_t rows,
+                                std::uint64_t cols, std::uint64_t seed, std::uint32_t p,
+                                int real) {
+    const std::uint64_t total = rows * cols;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+         i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t z = sm64_mix(seed + (i + 1) * 0x9e3779b97f4a7c15ull);
+        const std::uint64_t r = i / cols, c = i - r * cols;
+        double v;
+        if (real) v = 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
+        else v = static_cast<double>(z % p);
+        dst[r * ld + c] = v;
+    }
+}
+
+unsigned grid_for(std::uint64_t total) {
+    std::uint64_t b = (total + 255) / 256;
+    if (b > 148ull * 32) b = 148ull * 32;
+    return static_cast<unsigned>(b ? b : 1);
+}
+
+}  // namespace
+
+cudaError_t launch_addsub(const AddBatch& b, bool real, unsigned blocks, cudaStream_t s) {
+    if (real) k_addsub<true><<<blocks, kAddThreads, 0, s>>>(b);
+    else k_addsub<false><<<blocks, kAddThreads, 0, s>>>(b);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,
+                              std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
+                              cudaStream_t s) {
+    k_u32_to_f64<<<grid_for(rows * cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f64_to_u32(std::uint32_t* dst, std::uint64_t ldd, const double* src,
+                              std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
+                              std::uint32_t p, cudaStream_t s) {
+    k_f64_to_u32<<<grid_for(rows * cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols,
+                                                        static_cast<double>(p));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_splitmix(double* dst, std::uint64_t ld, std::uint64_t rows,
+                                 std::uint64_t cols, std::uint64_t seed, std::uint32_t p,
+                                 bool real, cudaStream_t s) {
+    k_fill_splitmix<<<grid_for(rows * cols), 256, 0, s>>>(dst, ld, rows, cols, seed, p,
+                                                           real ? 1 : 0);
+    return cudaGetLastError();
+}
+
+}  // namespace wm

@@ -1,0 +1,697 @@
+// Runtime and C-ABI (include/winomem_b200.h).
+//
+// A context owns one CUDA stream.  A call plans the multiplication on the host
+// (wm_planner.cpp), lowers the operation list to launches -- consecutive
+// independent additions are batched into one launch, leaves and fused frames
+// are one launch each -- and issues them in order on the stream.  Lowered plans
+// are cached per (variant, shape, scalars, pointers); with graphs enabled the
+// launch sequence of a cached plan is captured once into a CUDA graph and
+// replayed, which removes the per-launch host cost of the serial schedule chain.
+// Each cached plan owns a temporary arena of exactly its high-water size.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/winomem_b200.h"
+#include "wm_device.h"
+#include "wm_planner.h"
+
+namespace wm {
+cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s);      // wm_i8.cu
+cudaError_t launch_frame(const MulParams& P, bool real, cudaStream_t s);  // wm_frame.cu
+bool leaf_i8_supported(const MulParams& P);
+bool frame_supported(const MulParams& P, bool real);
+bool frame_kernel_available();
+}  // namespace wm
+
+using namespace wm;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_sched_calls;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define WM_CUDA(expr)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (expr);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            fail(E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+    } while (0)
+
+struct Step {
+    enum Kind : std::uint8_t { ADD, MUL, FRAME } kind;
+    AddBatch add;
+    unsigned blocks = 0;
+    MulParams mul;
+    int leaf = 0;  // MUL: 0 dmma, 1 i8
+};
+
+struct CachedPlan {
+    Plan plan;
+    std::vector<Step> steps;
+    double* arena = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~CachedPlan() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (arena) cudaFree(arena);
+    }
+};
+
+}  // namespace
+
+struct wm_ctx {
+    int device = 0;
+    Field f;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // options
+    bool fuse_frames = false;
+    bool graphs = true;
+    bool batch_adds = true;
+    int leaf_kernel = 0;  // 0 dmma, 1 i8, 2 auto
+    int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames
+    // plan cache (small LRU)
+    std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
+    // boundary staging
+    std::uint32_t* stage = nullptr;
+    std::size_t stage_words = 0;
+    double* hbuf[3] = {nullptr, nullptr, nullptr};
+    std::size_t hbuf_words[3] = {0, 0, 0};
+
+    ~wm_ctx() {
+        cache.clear();
+        if (stage) cudaFree(stage);
+        for (auto* b : hbuf)
+            if (b) cudaFree(b);
+        if (own_stream && stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+std::uint32_t modp_add_mode(const Field& f, Scalar sa, Scalar sb) {
+    const bool a1 = f.is_one(sa), am = f.is_minus_one(sa), b1 = f.is_one(sb),
+               bm = f.is_minus_one(sb);
+    if (a1 && b1) return M_ADD;
+    if (a1 && bm) return M_SUB;
+    if (am && b1) return M_RSUB;
+    if (am && bm) return M_NEGADD;
+    return M_GEN;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+AddItem make_item(const Op& op, const Field& f, double* const base[4]) {
+    AddItem t{};
+    t.d = base[op.d.region] + op.d.off;
+    t.a = base[op.a.region] + op.a.off;
+    t.ldd = op.d.ld;
+    t.lda = op.a.ld;
+    t.rows = static_cast<std::uint32_t>(op.d.rows);
+    t.cols = static_cast<std::uint32_t>(op.d.cols);
+    t.sa = op.sa.r;
+    t.sb = op.sb.r;
+    t.sad = op.sa.d;
+    t.sbd = op.sb.d;
+    bool vec = (t.cols % 2 == 0) && (t.ldd % 2 == 0) && (t.lda % 2 == 0) && aligned16(t.d) &&
+               aligned16(t.a);
+    if (op.kind == OP_ADDSUB) {
+        t.b = base[op.b.region] + op.b.off;
+        t.ldb = op.b.ld;
+        t.mode = modp_add_mode(f, op.sa, op.sb);
+        vec = vec && (t.ldb % 2 == 0) && aligned16(t.b);
+    } else {
+        t.b = t.a;
+        t.ldb = t.lda;
+        t.mode = f.is_one(op.sa) ? M_COPY : f.is_minus_one(op.sa) ? M_NEG : M_SCALE;
+    }
+    t.vec = vec ? 2 : 1;
+    return t;
+}
+
+unsigned item_blocks(const AddItem& t) {
+    const std::uint64_t units = static_cast<std::uint64_t>(t.rows) * t.cols / t.vec;
+    const std::uint64_t per = static_cast<std::uint64_t>(kAddThreads) * kAddIlp;
+    return static_cast<unsigned>((units + per - 1) / per);
+}
+
+MulParams make_mul(const Op& op, const Field& f, double* const base[4]) {
+    MulParams P{};
+    P.C = base[op.d.region] + op.d.off;
+    P.A = base[op.a.region] + op.a.off;
+    P.B = base[op.b.region] + op.b.off;
+    P.ldc = op.d.ld;
+    P.lda = op.a.ld;
+    P.ldb = op.b.ld;
+    P.m = static_cast<std::uint32_t>(op.a.rows);
+    P.k = static_cast<std::uint32_t>(op.a.cols);
+    P.n = static_cast<std::uint32_t>(op.b.cols);
+    P.alpha = op.sa.r;
+    P.beta = op.sb.r;
+    P.alphad = op.sa.d;
+    P.betad = op.sb.d;
+    P.p = f.p;
+    P.pd = static_cast<double>(f.p);
+    P.pinv = 1.0 / static_cast<double>(f.p);
+    return P;
+}
+
+void init_batch(AddBatch& b, const Field& f) {
+    std::memset(&b, 0, sizeof(b));
+    b.p = f.p;
+    b.pd = static_cast<double>(f.p);
+    b.pinv = 1.0 / static_cast<double>(f.p);
+}
+
+// Lower an operation list to launches.  Additions are merged into one launch
+// while they are pairwise independent (no write of one touches a read or
+// write of another) and contiguous in program order.
+std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& ctx) {
+    std::vector<Step> steps;
+    const Field& f = plan.field;
+    std::vector<const Op*> cur;
+    auto flush = [&]() {
+        if (cur.empty()) return;
+        Step s{};
+        s.kind = Step::ADD;
+        init_batch(s.add, f);
+        unsigned blk = 0;
+        for (const Op* op : cur) {
+            AddItem t = make_item(*op, f, base);
+            t.blk0 = blk;
+            blk += item_blocks(t);
+            s.add.it[s.add.n++] = t;
+        }
+        s.blocks = blk;
+        steps.push_back(s);
+        cur.clear();
+    };
+    auto conflicts = [&](const Op& o) {
+        for (const Op* c : cur) {
+            if (o.d.phys_overlaps(c->d) || o.d.phys_overlaps(c->a)) return true;
+            if (c->kind == OP_ADDSUB && o.d.phys_overlaps(c->b)) return true;
+            if (o.a.phys_overlaps(c->d)) return true;
+            if (o.kind == OP_ADDSUB && o.b.phys_overlaps(c->d)) return true;
+        }
+        return false;
+    };
+    for (const Op& op : plan.ops) {
+        if (op.kind == OP_ADDSUB || op.kind == OP_COPY) {
+            if (!ctx.batch_adds || static_cast<int>(cur.size()) >= kMaxAddBatch || conflicts(op))
+                flush();
+            cur.push_back(&op);
+            continue;
+        }
+        flush();
+        Step s{};
+        s.mul = make_mul(op, f, base);
+        if (op.kind == OP_FRAME) {
+            s.kind = Step::FRAME;
+        } else {
+            s.kind = Step::MUL;
+            const bool i8ok = !f.real && leaf_i8_supported(s.mul);
+            s.leaf = (ctx.leaf_kernel == 1 || ctx.leaf_kernel == 2) && i8ok ? 1 : 0;
+        }
+        steps.push_back(s);
+    }
+    flush();
+    return steps;
+}
+
+void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subset = 0) {
+    for (const Step& s : steps) {
+        if (subset == 1 && s.kind != Step::ADD) continue;
+        if (subset == 2 && s.kind != Step::MUL) continue;
+        if (subset == 3 && s.kind != Step::FRAME) continue;
+        switch (s.kind) {
+            case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
+            case Step::MUL:
+                if (s.leaf == 1) WM_CUDA(launch_leaf_i8(s.mul, st));
+                else WM_CUDA(launch_leaf_dmma(s.mul, real, st));
+                break;
+            case Step::FRAME: WM_CUDA(launch_frame(s.mul, real, st)); break;
+        }
+    }
+}
+
+void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r) {
+    if (!r) return;
+    std::memset(r, 0, sizeof(*r));
+    r->mults = plan.meter.mults;
+    r->adds = plan.meter.adds;
+    r->peak_extra_words = plan.meter.peak;
+    r->total_alloc_words = plan.meter.total;
+    r->word_moves = plan.meter.word_moves;
+    r->classical_calls = plan.meter.classical_calls;
+    for (const auto& kv : plan.meter.schedule_calls) r->schedule_frames += kv.second;
+    r->peak_extra_bytes = plan.arena_words * sizeof(double);
+    r->n_ops = plan.ops.size();
+    for (const auto& op : plan.ops) r->fused_frames += op.kind == OP_FRAME;
+    if (steps) r->n_launches = steps->size();
+    r->add_bytes = (3 * plan.meter.add2_elems + 2 * plan.meter.copy_elems) * sizeof(double);
+    r->leaf_flops = plan.meter.leaf_flops;
+    for (const auto& op : plan.ops) {
+        if (op.kind == OP_ADDSUB) r->add_bytes_issued += 3 * op.d.words() * sizeof(double);
+        if (op.kind == OP_COPY) r->add_bytes_issued += 2 * op.d.words() * sizeof(double);
+    }
+    std::ostringstream os;
+    bool first = true;
+    for (const auto& kv : plan.meter.schedule_calls) {
+        os << (first ? "" : ",") << kv.first << ":" << kv.second;
+        first = false;
+    }
+    g_sched_calls = os.str();
+}
+
+Scalar modp_scalar(const Field& f, std::uint32_t v) {
+    Scalar s;
+    s.r = v % f.p;
+    s.d = static_cast<double>(static_cast<std::int32_t>(v));  // REAL64 primitives: signed
+    return s;
+}
+Scalar real_scalar(double v) {
+    Scalar s;
+    s.r = 0;
+    s.d = v;
+    return s;
+}
+
+void check_dmat(const wm_dmat& m, const char* name) {
+    if (m.rows == 0 || m.cols == 0) fail(E_DIMENSION, std::string(name) + ": empty matrix");
+    if (m.ld < m.cols) fail(E_DIMENSION, std::string(name) + ": ld < cols");
+    if (!m.ptr) fail(E_INVALID, std::string(name) + ": null pointer");
+}
+
+void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dmat& B,
+         const wm_dmat& C, Scalar alpha, Scalar beta, int cutoff, wm_report* rep) {
+    check_dmat(A, "A");
+    check_dmat(B, "B");
+    check_dmat(C, "C");
+    if (B.rows != A.cols || C.rows != A.rows || C.cols != B.cols)
+        fail(E_DIMENSION, "multiply dimensions do not conform");
+    std::ostringstream key;
+    key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
+        << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
+        << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+    const std::string k = key.str();
+    CachedPlan* cp = nullptr;
+    for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
+        if (it->first == k) {
+            ctx->cache.splice(ctx->cache.begin(), ctx->cache, it);
+            cp = ctx->cache.front().second.get();
+            break;
+        }
+    if (!cp) {
+        PlanOptions opt;
+        opt.fuse_frames = ctx->fuse_frames && frame_kernel_available();
+        auto np = std::make_unique<CachedPlan>();
+        np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld, alpha,
+                                beta, cutoff, opt);
+        if (np->plan.arena_words)
+            WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
+        double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
+        np->steps = lower(np->plan, base, *ctx);
+        ctx->cache.emplace_front(k, std::move(np));
+        while (ctx->cache.size() > 8) ctx->cache.pop_back();
+        cp = ctx->cache.front().second.get();
+    }
+    if (ctx->graphs && cp->steps.size() > 1) {
+        if (!cp->exec) {
+            WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
+            } catch (...) {
+                cudaGraph_t g = nullptr;
+                cudaStreamEndCapture(ctx->stream, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            WM_CUDA(cudaStreamEndCapture(ctx->stream, &cp->graph));
+            WM_CUDA(cudaGraphInstantiate(&cp->exec, cp->graph, 0));
+        }
+        WM_CUDA(cudaGraphLaunch(cp->exec, ctx->stream));
+    } else {
+        issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
+    }
+    fill_report(cp->plan, &cp->steps, rep);
+}
+
+double* ensure_buf(wm_ctx* ctx, int i, std::size_t words) {
+    if (ctx->hbuf_words[i] < words) {
+        if (ctx->hbuf[i]) WM_CUDA(cudaFree(ctx->hbuf[i]));
+        ctx->hbuf[i] = nullptr;
+        WM_CUDA(cudaMalloc(&ctx->hbuf[i], words * sizeof(double)));
+        ctx->hbuf_words[i] = words;
+    }
+    return ctx->hbuf[i];
+}
+
+std::uint32_t* ensure_stage(wm_ctx* ctx, std::size_t words) {
+    if (ctx->stage_words < words) {
+        if (ctx->stage) WM_CUDA(cudaFree(ctx->stage));
+        ctx->stage = nullptr;
+        WM_CUDA(cudaMalloc(&ctx->stage, words * sizeof(std::uint32_t)));
+        ctx->stage_words = words;
+    }
+    return ctx->stage;
+}
+
+void upload(wm_ctx* ctx, const wm_dmat& dst, const std::uint32_t* host, std::uint64_t hld) {
+    check_dmat(dst, "dst");
+    std::uint32_t* st = ensure_stage(ctx, dst.rows * dst.cols);
+    WM_CUDA(cudaMemcpy2DAsync(st, dst.cols * 4, host, hld * 4, dst.cols * 4, dst.rows,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    WM_CUDA(launch_u32_to_f64(dst.ptr, dst.ld, st, dst.cols, dst.rows, dst.cols, ctx->stream));
+}
+
+void download(wm_ctx* ctx, std::uint32_t* host, std::uint64_t hld, const wm_dmat& src) {
+    check_dmat(src, "src");
+    std::uint32_t* st = ensure_stage(ctx, src.rows * src.cols);
+    WM_CUDA(launch_f64_to_u32(st, src.cols, src.ptr, src.ld, src.rows, src.cols, ctx->f.p,
+                              ctx->stream));
+    WM_CUDA(cudaMemcpy2DAsync(host, hld * 4, st, src.cols * 4, src.cols * 4, src.rows,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+template <class F>
+int guard(F&& fn) {
+    try {
+        fn();
+        return WM_OK;
+    } catch (const Error& e) {
+        return set_err(e.code, e.what());
+    } catch (const std::exception& e) {
+        return set_err(E_INVALID, e.what());
+    }
+}
+
+// Primitive calls on raw pointers: all device memory is one "region"; views
+// over distinct allocations never overlap physically, so the exact /
+// span tests of MatView::overlaps apply to the addresses directly.
+View raw_view(const wm_dmat& m) {
+    View v;
+    v.region = 0;
+    v.origin = 0;
+    v.base = 0;
+    v.off = reinterpret_cast<std::uintptr_t>(m.ptr) / sizeof(double);
+    v.rows = m.rows;
+    v.cols = m.cols;
+    v.ld = m.ld;
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* wm_version(void) { return "winomem-b200 0.1 (sm_100a)"; }
+const char* wm_last_error(void) { return g_err.c_str(); }
+
+int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out) {
+    return guard([&] {
+        if (!out) fail(E_INVALID, "null out");
+        *out = nullptr;
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+            fail(E_CUDA, "no CUDA device: winomem-b200 has no CPU fallback");
+        if (device < 0 || device >= n) fail(E_INVALID, "bad device ordinal");
+        if (field != WM_FIELD_MODP && field != WM_FIELD_REAL64) fail(E_INVALID, "bad field");
+        if (field == WM_FIELD_MODP) {
+            bool prime = p > 2 && (p & 1);
+            for (std::uint32_t d = 3; prime && static_cast<std::uint64_t>(d) * d <= p; d += 2)
+                prime = p % d != 0;
+            if (!prime) fail(E_DIMENSION, "modulus must be an odd prime: " + std::to_string(p));
+            if (p >= (1u << 16))
+                fail(E_DIMENSION, "device path supports p < 2^16 (exact float64 accumulation)");
+        }
+        auto c = std::make_unique<wm_ctx>();
+        c->device = device;
+        c->f.real = field == WM_FIELD_REAL64;
+        c->f.p = field == WM_FIELD_REAL64 ? 65521u : p;
+        WM_CUDA(cudaSetDevice(device));
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+        } else {
+            WM_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->own_stream = true;
+        }
+        *out = c.release();
+    });
+}
+
+int wm_ctx_destroy(wm_ctx* ctx) {
+    if (ctx) {
+        cudaStreamSynchronize(ctx->stream);
+        delete ctx;
+    }
+    return WM_OK;
+}
+
+int wm_ctx_sync(wm_ctx* ctx) {
+    return guard([&] { WM_CUDA(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
+    return guard([&] {
+        const std::string k = key ? key : "";
+        if (k == "fuse_frames") ctx->fuse_frames = value != 0;
+        else if (k == "graphs") ctx->graphs = value != 0;
+        else if (k == "batch_adds") ctx->batch_adds = value != 0;
+        else if (k == "leaf_kernel") ctx->leaf_kernel = static_cast<int>(value);
+        else if (k == "subset") ctx->subset = static_cast<int>(value);
+        else fail(E_INVALID, "unknown option " + k);
+        ctx->cache.clear();
+    });
+}
+
+int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
+    return guard([&] {
+        const std::string k = key ? key : "";
+        if (k == "fuse_frames") *value = ctx->fuse_frames;
+        else if (k == "graphs") *value = ctx->graphs;
+        else if (k == "batch_adds") *value = ctx->batch_adds;
+        else if (k == "leaf_kernel") *value = ctx->leaf_kernel;
+        else if (k == "subset") *value = ctx->subset;
+        else fail(E_INVALID, "unknown option " + k);
+    });
+}
+
+int wm_block_addsub(wm_ctx* ctx, wm_dmat dst, wm_dmat a, wm_dmat b, uint32_t sa, uint32_t sb) {
+    return guard([&] {
+        check_dmat(dst, "dst");
+        check_dmat(a, "a");
+        check_dmat(b, "b");
+        const View d = raw_view(dst), va = raw_view(a), vb = raw_view(b);
+        if (a.rows != b.rows || a.cols != b.cols || dst.rows != a.rows || dst.cols != a.cols)
+            fail(E_DIMENSION, "block_addsub dimension mismatch");
+        if (!d.same_window(va) && d.overlaps(va))
+            fail(E_PARTIAL_OVERLAP, "block_addsub: dst partially overlaps a");
+        if (!d.same_window(vb) && d.overlaps(vb))
+            fail(E_PARTIAL_OVERLAP, "block_addsub: dst partially overlaps b");
+        Op op{};
+        op.kind = OP_ADDSUB;
+        op.d = d;
+        op.a = va;
+        op.b = vb;
+        op.sa = modp_scalar(ctx->f, sa);
+        op.sb = modp_scalar(ctx->f, sb);
+        // raw views are absolute element addresses from a null base
+        op.d.region = op.a.region = op.b.region = 0;
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        Step s{};
+        s.kind = Step::ADD;
+        init_batch(s.add, ctx->f);
+        AddItem t = make_item(op, ctx->f, base);
+        t.blk0 = 0;
+        s.add.it[0] = t;
+        s.add.n = 1;
+        s.blocks = item_blocks(t);
+        WM_CUDA(launch_addsub(s.add, ctx->f.real, s.blocks, ctx->stream));
+    });
+}
+
+int wm_block_scale_copy(wm_ctx* ctx, wm_dmat dst, wm_dmat src, uint32_t s) {
+    return guard([&] {
+        check_dmat(dst, "dst");
+        check_dmat(src, "src");
+        const View d = raw_view(dst), v = raw_view(src);
+        if (dst.rows != src.rows || dst.cols != src.cols)
+            fail(E_DIMENSION, "block_scale_copy dimension mismatch");
+        if (!d.same_window(v) && d.overlaps(v))
+            fail(E_PARTIAL_OVERLAP, "block_scale_copy: dst partially overlaps src");
+        if (s % ctx->f.p == 1 && d.same_window(v)) return;
+        Op op{};
+        op.kind = OP_COPY;
+        op.d = d;
+        op.a = v;
+        op.sa = modp_scalar(ctx->f, s);
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        Step st{};
+        init_batch(st.add, ctx->f);
+        AddItem t = make_item(op, ctx->f, base);
+        st.add.it[0] = t;
+        st.add.n = 1;
+        WM_CUDA(launch_addsub(st.add, ctx->f.real, item_blocks(t), ctx->stream));
+    });
+}
+
+int wm_classical_mul(wm_ctx* ctx, wm_dmat C, wm_dmat A, wm_dmat B, uint32_t alpha, uint32_t beta) {
+    return guard([&] {
+        check_dmat(A, "A");
+        check_dmat(B, "B");
+        check_dmat(C, "C");
+        if (B.rows != A.cols || C.rows != A.rows || C.cols != B.cols)
+            fail(E_DIMENSION, "classical_mul dimension mismatch");
+        const View vc = raw_view(C);
+        if (vc.overlaps(raw_view(A)) || vc.overlaps(raw_view(B)))
+            fail(E_ALIAS, "classical_mul: C must be disjoint from A and B");
+        Op op{};
+        op.kind = OP_MUL;
+        op.d = vc;
+        op.a = raw_view(A);
+        op.b = raw_view(B);
+        op.sa = modp_scalar(ctx->f, alpha);
+        op.sb = modp_scalar(ctx->f, beta);
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        MulParams P = make_mul(op, ctx->f, base);
+        if (!ctx->f.real && (ctx->leaf_kernel == 1 || ctx->leaf_kernel == 2) && leaf_i8_supported(P))
+            WM_CUDA(launch_leaf_i8(P, ctx->stream));
+        else
+            WM_CUDA(launch_leaf_dmma(P, ctx->f.real, ctx->stream));
+    });
+}
+
+int wm_run_variant(wm_ctx* ctx, const char* variant, wm_dmat A, wm_dmat B, wm_dmat C,
+                   uint32_t alpha, uint32_t beta, int cutoff, wm_report* report) {
+    return guard([&] {
+        if (ctx->f.real) fail(E_INVALID, "REAL64 context: use wm_run_variant_real");
+        run(ctx, variant ? variant : "", A, B, C, modp_scalar(ctx->f, alpha),
+            modp_scalar(ctx->f, beta), cutoff, report);
+    });
+}
+
+int wm_ipmm(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int cutoff, wm_report* report) {
+    return wm_run_variant(ctx, "ipmm", A, B, C, 1, 0, cutoff, report);
+}
+
+int wm_run_variant_real(wm_ctx* ctx, const char* variant, wm_dmat A, wm_dmat B, wm_dmat C,
+                        double alpha, double beta, int cutoff, wm_report* report) {
+    return guard([&] {
+        if (!ctx->f.real) fail(E_INVALID, "MODP context: use wm_run_variant");
+        run(ctx, variant ? variant : "", A, B, C, real_scalar(alpha), real_scalar(beta), cutoff,
+            report);
+    });
+}
+
+int wm_run_variant_host_u32(wm_ctx* ctx, const char* variant, uint64_t m, uint64_t k, uint64_t n,
+                            uint32_t* A, uint32_t* B, uint32_t* C, uint32_t alpha, uint32_t beta,
+                            int cutoff, wm_report* report) {
+    return guard([&] {
+        if (ctx->f.real) fail(E_INVALID, "host u32 entry needs a MODP context");
+        if (!A || !B || !C) fail(E_INVALID, "null host buffer");
+        const std::string v = variant ? variant : "";
+        wm_dmat dA{ensure_buf(ctx, 0, m * k), m, k, k};
+        wm_dmat dB{ensure_buf(ctx, 1, k * n), k, n, n};
+        wm_dmat dC{ensure_buf(ctx, 2, m * n), m, n, n};
+        upload(ctx, dA, A, k);
+        upload(ctx, dB, B, n);
+        if (beta % ctx->f.p != 0) upload(ctx, dC, C, n);
+        run(ctx, v, dA, dB, dC, modp_scalar(ctx->f, alpha), modp_scalar(ctx->f, beta), cutoff,
+            report);
+        download(ctx, C, n, dC);
+        const Contract c = variant_contract(v);
+        if (c == Contract::OverwriteA || c == Contract::OverwriteBoth) download(ctx, A, k, dA);
+        if (c == Contract::OverwriteB || c == Contract::OverwriteBoth) download(ctx, B, n, dB);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int wm_plan_report(const char* variant, int field, uint32_t p, uint64_t m, uint64_t k, uint64_t n,
+                   uint32_t alpha, uint32_t beta, int cutoff, int fuse_frames, wm_report* report) {
+    return guard([&] {
+        Field f;
+        f.real = field == WM_FIELD_REAL64;
+        f.p = f.real ? 65521u : p;
+        PlanOptions opt;
+        opt.fuse_frames = fuse_frames != 0;
+        Scalar a = f.real ? real_scalar(alpha) : modp_scalar(f, alpha);
+        Scalar b = f.real ? real_scalar(beta) : modp_scalar(f, beta);
+        Plan plan = plan_variant(variant ? variant : "", f, m, k, n, k, n, n, a, b, cutoff, opt);
+        fill_report(plan, nullptr, report);
+        if (report) {
+            // launches as lowered with batching (pointer-free count)
+            wm_ctx dummy;
+            dummy.batch_adds = true;
+            double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+            report->n_launches = lower(plan, base, dummy).size();
+        }
+    });
+}
+
+int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, int cutoff,
+                      wm_report* report) {
+    return guard([&] {
+        Costs c = expected_costs(variant ? variant : "", m, k, n, cutoff);
+        if (report) {
+            std::memset(report, 0, sizeof(*report));
+            report->mults = c.mults;
+            report->adds = c.adds;
+            report->peak_extra_words = c.peak;
+            report->total_alloc_words = c.total;
+            report->word_moves = c.moves;
+        }
+    });
+}
+
+int wm_plan_schedule_calls(char* out, int len) {
+    if (out && len > 0) {
+        std::strncpy(out, g_sched_calls.c_str(), static_cast<std::size_t>(len) - 1);
+        out[len - 1] = 0;
+    }
+    return static_cast<int>(g_sched_calls.size());
+}
+
+int wm_upload_u32(wm_ctx* ctx, wm_dmat dst, const uint32_t* host, uint64_t host_ld) {
+    return guard([&] { upload(ctx, dst, host, host_ld); });
+}
+
+int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src) {
+    return guard([&] {
+        download(ctx, host, host_ld, src);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+uint64_t wm_fnv1a64_u32(const uint32_t* data, uint64_t count) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (std::uint64_t i = 0; i < count; ++i) {
+        h ^= data[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+int wm_fill_random(wm_ctx* ctx, wm_dmat dst, uint64_t seed) {
+    return guard([&] {
+        check_dmat(dst, "dst");
+        WM_CUDA(launch_fill_splitmix(dst.ptr, dst.ld, dst.rows, dst.cols, seed, ctx->f.p,
+                                     ctx->f.real, ctx->stream));
+    });
+}
+
+}  // extern "C"

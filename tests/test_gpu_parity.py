@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path through the C-ABI against the reference's golden
+results (bit-exact, mod p) and the CPU oracle.  Needs a B200."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ACC = {"acc3", "aclr", "accr", "acc2", "acr"}
+
+
+def _acc(v):
+    return v in ACC or v.startswith("blocked")
+
+
+def _contract_keeps(v):
+    """(A preserved, B preserved) by the variant's contract (acceptance.cpp:104-110)."""
+    if v in ("ipovmm", "iprect"):
+        return False, False
+    if v in ("ipmm", "classic") or v.startswith("blocked"):
+        return True, True
+    c = {"std2": "ro", "acc3": "ro", "acc2": "ro", "ip": "both", "aclr": "both", "ovl": "A",
+         "ovl2": "A", "ovr": "B", "accr": "B", "acr": "B"}[v]
+    return c in ("ro", "B"), c in ("ro", "A")
+
+
+def _problem(W, m, k, n, seed, acc):
+    A, B, C = W.Matrix(m, k), W.Matrix(k, n), W.Matrix(m, n)
+    A.fill_random(seed)
+    B.fill_random(seed + 1)
+    if acc:
+        C.fill_random(seed + 2)
+    return A, B, C
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return json.load(open(os.path.join(GOLD, "small_cases.json")))["cases"]
+
+
+@pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0), dict(fuse_frames=1),
+                        dict(leaf_kernel=1), dict(leaf_kernel=1, fuse_frames=1)],
+                ids=["default", "nograph", "fused", "i8", "i8-fused"])
+def options(request, W):
+    ctx = W.Context.get()
+    saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
+                                              "leaf_kernel")}
+    for k, v in request.param.items():
+        ctx.set_option(k, v)
+    yield request.param
+    for k, v in saved.items():
+        ctx.set_option(k, v)
+
+
+def test_device_generator_matches_fill_random(W, O):
+    for (r, c, seed) in [(1, 1, 1), (3, 5, 9), (64, 48, 2), (257, 129, 77)]:
+        M = W.Matrix(r, c)
+        M.fill_random(seed)
+        assert (M.to_u32() == O.fill_random(r, c, seed)).all()
+
+
+def test_golden_small_cases(W, golden, options):
+    seen = 0
+    for c in golden:
+        if c["seed"] != 11 and options:
+            continue  # option sweeps replay one seed; the default replays all
+        v, m, k, n = c["variant"], c["m"], c["k"], c["n"]
+        A, B, C = _problem(W, m, k, n, c["seed"], _acc(v))
+        if "error" in c:
+            with pytest.raises(W.winomem.WinomemError) as ei:
+                W.run_variant(v, A, B, C, alpha=c["alpha"], beta=c["beta"], cutoff=c["cutoff"])
+            assert ei.value.code == c["error"]
+            continue
+        rep = W.run_variant(v, A, B, C, alpha=c["alpha"], beta=c["beta"], cutoff=c["cutoff"])
+        assert "%016x" % C.hash() == c["c_hash"], c
+        ka, kb = _contract_keeps(v)
+        if ka:
+            assert "%016x" % A.hash() == c["a_before"], ("A clobbered", c)
+        if kb:
+            assert "%016x" % B.hash() == c["b_before"], ("B clobbered", c)
+        assert rep.mults == c["report"]["mults"] and rep.adds == c["report"]["adds"]
+        assert rep.peak_extra_words == c["report"]["peak_extra_words"]
+        seen += 1
+    assert seen > 300
+
+
+def test_primitive_kats(W):
+    E = W.winomem
+    a = W.Matrix(2, 2, W.Modulus(65521)).from_u32(np.array([[1, 2], [3, 4]], dtype=np.uint32))
+    b = W.Matrix(2, 2).from_u32(np.array([[5, 6], [65520, 8]], dtype=np.uint32))
+    d = W.Matrix(2, 2)
+    W.block_addsub(d.view(), a.view(), b.view(), 1, 1)
+    assert d.to_u32().tolist() == [[6, 8], [2, 12]]
+    W.block_addsub(d.view(), a.view(), a.view(), 1, 65520)
+    assert (d.to_u32() == 0).all()
+    W.block_addsub(d.view(), a.view(), b.view(), 3, 95)
+    want = (3 * np.array([[1, 2], [3, 4]]) + 95 * np.array([[5, 6], [65520, 8]])) % 65521
+    assert (d.to_u32() == want).all()
+    C = W.Matrix(2, 2)
+    W.classical_mul(C.view(), a.view(), b.view(), 1, 0)
+    want = (np.array([[1, 2], [3, 4]]) @ np.array([[5, 6], [65520, 8]])) % 65521
+    assert (C.to_u32() == want).all()
+    big = W.Matrix(4, 4)
+    q = W.quad_split(big.view())
+    with pytest.raises(E.partial_overlap_error):
+        W.block_addsub(big.view().window(1, 1, 2, 2), q[0], q[0], 1, 1)
+    W.block_addsub(q[0], q[0], q[3], 1, 1)  # exact aliasing is allowed
+    with pytest.raises(E.alias_error):
+        W.classical_mul(a.view(), a.view(), a.view(), 1, 0)
+
+
+def test_classical_vs_oracle_random_shapes(W, O, options):
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        m, k, n = (int(x) for x in rng.integers(1, 300, 3))
+        al, be = int(rng.integers(0, 65521)), int(rng.integers(0, 65521))
+        A, B, C = _problem(W, m, k, n, int(rng.integers(1, 1 << 30)), True)
+        a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+        W.classical_mul(C.view(), A.view(), B.view(), al, be)
+        assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (m, k, n)
+
+
+@pytest.mark.parametrize("v", ["std2", "acc3", "ip", "ovl", "ovr", "aclr", "accr", "acc2",
+                               "ipmm", "iprect"])
+def test_midsize_vs_oracle(W, O, v, options):
+    """512..1024-sized problems at cutoffs 64/128 vs the oracle classical product."""
+    for (m, k, n, c) in [(512, 512, 512, 64), (1024, 1024, 1024, 128)]:
+        if v == "iprect":
+            m, n = 2 * m, 2 * n
+        A, B, C = _problem(W, m, k, n, 101 + m, _acc(v))
+        a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+        W.run_variant(v, A, B, C, alpha=1, beta=1 if _acc(v) else 0, cutoff=c)
+        want = O.classical_modp(a0, b0, c0 if _acc(v) else None, 1, 1 if _acc(v) else 0)
+        assert (C.to_u32() == want).all(), (v, m, k, n, c, options)
+
+
+CFG = json.load(open(os.path.join(GOLD, "config_hashes.json")))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_config_full_size_hash(W, name):
+    if name not in CFG:
+        pytest.skip("hash not generated")
+    c = CFG[name]
+    want = c["appendix_a"]
+    A, B, C = _problem(W, c["m"], c["k"], c["n"], c["seed"], bool(c["beta"]))
+    rep = W.run_variant(c["variant"], A, B, C, alpha=c["alpha"], beta=c["beta"],
+                        cutoff=c["cutoff"])
+    assert "%016x" % C.hash() == want
+    e = W.expected_costs(c["variant"], c["m"], c["k"], c["n"], c["cutoff"])
+    assert rep.peak_extra_words == e.peak_extra_words
+    assert rep.peak_extra_bytes == 8 * e.peak_extra_words
+
+
+def test_host_u32_end_to_end(W, O):
+    A, B = O.fill_random(1024, 1024, 1), O.fill_random(1024, 1024, 2)
+    C = np.zeros((1024, 1024), dtype=np.uint32)
+    rep = W.run_variant_host("std2", A, B, C, cutoff=128)
+    assert "%016x" % O.fnv1a64(C) == CFG["C1"]["hash"]
+    assert rep.peak_extra_words == 688128
+    # accumulating, with host C in/out
+    A, B, C0 = O.fill_random(256, 256, 5), O.fill_random(256, 256, 6), O.fill_random(256, 256, 7)
+    Cm = C0.copy()
+    W.run_variant_host("acc2", A, B, Cm, alpha=3, beta=7, cutoff=32)
+    assert (Cm == O.classical_modp(A, B, C0, 3, 7)).all()
+
+
+def test_real64_winograd_frobenius(W, O):
+    """Config-5 field: float64 std2 vs the oracle classical float64 product.
+    Stated tolerance: relative Frobenius error <= 1e-12 * 2^depth."""
+    for (n, cutoff) in [(1024, 128), (2048, 64)]:
+        depth = (n // cutoff).bit_length() - 1
+        A = W.Matrix(n, n, real=True)
+        B = W.Matrix(n, n, real=True)
+        C = W.Matrix(n, n, real=True)
+        A.fill_random(5)
+        B.fill_random(6)
+        W.run_variant("std2", A, B, C, cutoff=cutoff)
+        a = O.real_fill(n, n, 5)
+        b = O.real_fill(n, n, 6)
+        assert np.array_equal(A.t.cpu().numpy(), a)
+        ref = O.classical_f64(a, b)
+        got = C.t.cpu().numpy()
+        err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+        assert err <= 1e-12 * 2 ** depth, (n, cutoff, err)
