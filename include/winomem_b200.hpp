@@ -1,0 +1,367 @@
+// winomem-b200 C++ drop-in: the reference winomem API (namespace winomem,
+// /root/reference/proj/include/winomem/) re-declared over the C-ABI in
+// winomem_b200.h.  Code written against the reference's run_variant / multiply /
+// ipmm / classical_mul / block_addsub / models::expected_costs compiles
+// unchanged against this header and runs on the B200; link with
+// libwinomem_b200.so.
+//
+// Matrices stay host-resident uint32 residues exactly as in the reference
+// (ring.hpp:180-219); every call uploads, runs on the device and writes back the
+// matrices the variant's contract allows it to change.  Errors are thrown as
+// the reference's exception types.  There is no CPU path: without a CUDA
+// device the calls throw.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "winomem_b200.h"
+
+namespace winomem {
+
+using Elem = std::uint32_t;
+
+// ---- exception taxonomy (ring.hpp:23-43, workspace.hpp:20-22, schedule.hpp:30-43)
+struct dimension_error : std::runtime_error {
+    explicit dimension_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct odd_dimension_error : dimension_error {
+    explicit odd_dimension_error(const std::string& w) : dimension_error(w) {}
+};
+struct partial_overlap_error : std::runtime_error {
+    explicit partial_overlap_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct alias_error : std::runtime_error {
+    explicit alias_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct shape_error : std::runtime_error {
+    explicit shape_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct contract_error : std::runtime_error {
+    explicit contract_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct io_error : std::runtime_error {
+    explicit io_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct workspace_error : std::runtime_error {
+    explicit workspace_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct unknown_schedule_error : std::runtime_error {
+    explicit unknown_schedule_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct parse_error : std::runtime_error {
+    explicit parse_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct contract_violation_error : std::runtime_error {
+    explicit contract_violation_error(const std::string& w) : std::runtime_error(w) {}
+};
+struct device_error : std::runtime_error {
+    explicit device_error(const std::string& w) : std::runtime_error(w) {}
+};
+
+namespace b200 {
+inline void check(int rc) {
+    if (rc == WM_OK) return;
+    const std::string w = wm_last_error();
+    switch (rc) {
+        case WM_E_DIMENSION: throw dimension_error(w);
+        case WM_E_ODD_DIMENSION: throw odd_dimension_error(w);
+        case WM_E_PARTIAL_OVERLAP: throw partial_overlap_error(w);
+        case WM_E_ALIAS: throw alias_error(w);
+        case WM_E_SHAPE: throw shape_error(w);
+        case WM_E_CONTRACT: throw contract_error(w);
+        case WM_E_IO: throw io_error(w);
+        case WM_E_WORKSPACE: throw workspace_error(w);
+        case WM_E_UNKNOWN_SCHEDULE: throw unknown_schedule_error(w);
+        case WM_E_PARSE: throw parse_error(w);
+        case WM_E_CONTRACT_VIOLATION: throw contract_violation_error(w);
+        default: throw device_error(w);
+    }
+}
+
+inline int& device_ordinal() {
+    static int d = 0;
+    return d;
+}
+inline void set_device(int d) { device_ordinal() = d; }
+
+// one context per modulus, created on first use
+inline wm_ctx* context(std::uint32_t p) {
+    static std::mutex mu;
+    static std::map<std::uint32_t, wm_ctx*> ctxs;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = ctxs.find(p);
+    if (it != ctxs.end()) return it->second;
+    wm_ctx* c = nullptr;
+    check(wm_ctx_create(device_ordinal(), p, WM_FIELD_MODP, nullptr, &c));
+    ctxs[p] = c;
+    return c;
+}
+}  // namespace b200
+
+// ---- ring (ring.hpp:47-228) ----------------------------------------------
+class Modulus {
+  public:
+    explicit Modulus(std::uint32_t p) : p_(p) {
+        if (p <= 2 || p >= (1u << 31) || !is_prime(p))
+            throw dimension_error("modulus must be an odd prime in (2, 2^31): " + std::to_string(p));
+    }
+    std::uint32_t p() const { return p_; }
+    Elem minus_one() const { return p_ - 1; }
+    Elem add(Elem a, Elem b) const { std::uint32_t s = a + b; return s >= p_ ? s - p_ : s; }
+    Elem sub(Elem a, Elem b) const { return a >= b ? a - b : a + p_ - b; }
+    Elem neg(Elem a) const { return a ? p_ - a : 0; }
+    Elem mul(Elem a, Elem b) const {
+        return static_cast<Elem>(static_cast<std::uint64_t>(a) * b % p_);
+    }
+    bool operator==(const Modulus& o) const { return p_ == o.p_; }
+    static bool is_prime(std::uint32_t n) {
+        if (n < 2) return false;
+        if (n % 2 == 0) return n == 2;
+        for (std::uint64_t d = 3; d * d <= n; d += 2)
+            if (n % d == 0) return false;
+        return true;
+    }
+
+  private:
+    std::uint32_t p_;
+};
+
+inline constexpr std::uint32_t kDefaultModulus = 65521;
+
+class SplitMix64 {
+  public:
+    explicit SplitMix64(std::uint64_t seed) : state_(seed) {}
+    std::uint64_t next() {
+        std::uint64_t z = (state_ += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+
+  private:
+    std::uint64_t state_;
+};
+
+inline std::uint64_t fnv1a64(const Elem* data, std::size_t count) {
+    return wm_fnv1a64_u32(data, count);
+}
+
+struct MatView {
+    Elem* ptr = nullptr;
+    std::size_t rows = 0, cols = 0, stride = 0;
+    const Elem* origin = nullptr;
+    Elem& at(std::size_t i, std::size_t j) const { return ptr[i * stride + j]; }
+    std::size_t words() const { return rows * cols; }
+    MatView window(std::size_t r0, std::size_t c0, std::size_t r, std::size_t c) const {
+        if (r0 + r > rows || c0 + c > cols) throw dimension_error("window exceeds view bounds");
+        return MatView{ptr + r0 * stride + c0, r, c, stride, origin};
+    }
+};
+
+class Matrix {
+  public:
+    Matrix(std::size_t rows, std::size_t cols, Modulus mod)
+        : rows_(rows), cols_(cols), mod_(mod), data_(rows * cols, 0) {
+        if (rows == 0 || cols == 0) throw dimension_error("matrix dimensions must be positive");
+    }
+    std::size_t rows() const { return rows_; }
+    std::size_t cols() const { return cols_; }
+    const Modulus& mod() const { return mod_; }
+    Elem* data() { return data_.data(); }
+    const Elem* data() const { return data_.data(); }
+    std::size_t size() const { return data_.size(); }
+    Elem& at(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
+    Elem at(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
+    MatView view() { return MatView{data_.data(), rows_, cols_, cols_, data_.data()}; }
+    void fill_random(std::uint64_t seed) {
+        SplitMix64 g(seed);
+        for (auto& x : data_) x = static_cast<Elem>(g.next() % mod_.p());
+    }
+    void fill_zero() { std::fill(data_.begin(), data_.end(), 0); }
+    std::uint64_t hash() const { return fnv1a64(data_.data(), data_.size()); }
+    bool operator==(const Matrix& o) const {
+        return rows_ == o.rows_ && cols_ == o.cols_ && mod_ == o.mod_ && data_ == o.data_;
+    }
+
+  private:
+    std::size_t rows_, cols_;
+    Modulus mod_;
+    std::vector<Elem> data_;
+};
+
+// ---- meter (meter.hpp) -----------------------------------------------------
+class CostMeter {
+  public:
+    std::uint64_t mults = 0, adds = 0, word_moves = 0;
+    std::uint64_t live_extra_words = 0, peak_extra_words = 0, total_alloc_words = 0;
+    std::uint64_t classical_calls = 0;
+    std::map<std::string, std::uint64_t> schedule_calls;
+    // device figures of the last call
+    std::uint64_t peak_extra_bytes = 0, launches = 0;
+};
+
+struct CostReport {
+    std::string variant;
+    std::size_t m = 0, k = 0, n = 0;
+    int cutoff = 1;
+    std::uint64_t mults = 0, adds = 0, peak_extra_words = 0, total_alloc_words = 0,
+                  word_moves = 0;
+    std::uint64_t ops() const { return mults + adds; }
+    static const char* csv_header() { return "variant,m,k,n,cutoff,mults,adds,peak_extra,total_alloc"; }
+    std::string csv_row() const {
+        std::ostringstream os;
+        os << variant << ',' << m << ',' << k << ',' << n << ',' << cutoff << ',' << mults << ','
+           << adds << ',' << peak_extra_words << ',' << total_alloc_words;
+        return os.str();
+    }
+};
+
+struct DiffReport {
+    std::vector<std::string> diffs;
+    bool empty() const { return diffs.empty(); }
+};
+
+inline DiffReport compare(const CostReport& a, const CostReport& b) {
+    DiffReport r;
+    auto chk = [&](const char* f, std::uint64_t x, std::uint64_t y) {
+        if (x != y) r.diffs.push_back(std::string(f) + ": measured=" + std::to_string(x) +
+                                      " expected=" + std::to_string(y));
+    };
+    chk("mults", a.mults, b.mults);
+    chk("adds", a.adds, b.adds);
+    chk("peak_extra_words", a.peak_extra_words, b.peak_extra_words);
+    chk("total_alloc_words", a.total_alloc_words, b.total_alloc_words);
+    return r;
+}
+
+struct MultiplyOptions {
+    Elem alpha = 1;
+    Elem beta = 0;
+    int cutoff = 1;
+};
+
+namespace b200 {
+inline CostReport to_report(const std::string& v, std::size_t m, std::size_t k, std::size_t n,
+                            int cutoff, const wm_report& r, CostMeter* meter) {
+    CostReport rep;
+    rep.variant = v;
+    rep.m = m;
+    rep.k = k;
+    rep.n = n;
+    rep.cutoff = cutoff;
+    rep.mults = r.mults;
+    rep.adds = r.adds;
+    rep.peak_extra_words = r.peak_extra_words;
+    rep.total_alloc_words = r.total_alloc_words;
+    rep.word_moves = r.word_moves;
+    if (meter) {
+        meter->mults += r.mults;
+        meter->adds += r.adds;
+        meter->word_moves += r.word_moves;
+        meter->peak_extra_words = std::max(meter->peak_extra_words, r.peak_extra_words);
+        meter->total_alloc_words += r.total_alloc_words;
+        meter->classical_calls += r.classical_calls;
+        meter->peak_extra_bytes = r.peak_extra_bytes;
+        meter->launches = r.n_launches;
+        char buf[4096];
+        wm_plan_schedule_calls(buf, sizeof(buf));
+        std::string s(buf), item;
+        std::istringstream is(s);
+        while (std::getline(is, item, ',')) {
+            auto c = item.find(':');
+            if (c != std::string::npos)
+                meter->schedule_calls[item.substr(0, c)] += std::stoull(item.substr(c + 1));
+        }
+    }
+    return rep;
+}
+}  // namespace b200
+
+// run_variant (drivers.hpp:213-222) -- executes on the B200
+inline CostReport run_variant(const std::string& variant, Matrix& A, Matrix& B, Matrix& C,
+                              const MultiplyOptions& opt = {}, CostMeter* meter = nullptr) {
+    if (!(A.mod() == B.mod()) || !(A.mod() == C.mod()))
+        throw dimension_error("operands use different moduli");
+    if (B.rows() != A.cols() || C.rows() != A.rows() || C.cols() != B.cols())
+        throw dimension_error("multiply dimensions do not conform");
+    wm_report r{};
+    b200::check(wm_run_variant_host_u32(b200::context(A.mod().p()), variant.c_str(), A.rows(),
+                                        A.cols(), B.cols(), A.data(), B.data(), C.data(),
+                                        opt.alpha, opt.beta, opt.cutoff, &r));
+    return b200::to_report(variant, A.rows(), A.cols(), B.cols(), opt.cutoff, r, meter);
+}
+
+// multiply (executor.hpp:240-299)
+inline CostReport multiply(const std::string& variant, Matrix& A, Matrix& B, Matrix& C,
+                           const MultiplyOptions& opt = {}, CostMeter* meter = nullptr) {
+    return run_variant(variant, A, B, C, opt, meter);
+}
+
+// ipmm / ipovmm (drivers.hpp:52-158)
+inline CostReport ipmm(Matrix& A, Matrix& B, Matrix& C, int cutoff = 1, CostMeter* meter = nullptr) {
+    return run_variant("ipmm", A, B, C, {1, 0, cutoff}, meter);
+}
+inline CostReport ipovmm(Matrix& A, Matrix& B, Matrix& C, int cutoff = 1,
+                         CostMeter* meter = nullptr) {
+    return run_variant("ipovmm", A, B, C, {1, 0, cutoff}, meter);
+}
+inline CostReport blocked_acc(Matrix& A, Matrix& B, Matrix& C, Elem alpha, Elem beta, int t,
+                              const std::string& base = "acc3", int cutoff = 1,
+                              CostMeter* meter = nullptr) {
+    const std::string v = "blocked_acc_t" + std::to_string(t) + (base == "acc2" ? "_acc2" : "");
+    if (base != "acc3" && base != "acc2")
+        throw unknown_schedule_error("blocked_acc base must be acc3 or acc2");
+    return run_variant(v, A, B, C, {alpha, beta, cutoff}, meter);
+}
+
+// classical_mul (ring.hpp:315-384) on whole matrices
+inline void classical_mul(Matrix& C, Matrix& A, Matrix& B, Elem alpha, Elem beta) {
+    run_variant("classic", A, B, C, {alpha, beta, 1});
+}
+
+namespace models {
+// expected_costs (models.hpp:202-229)
+inline CostReport expected_costs(const std::string& variant, std::size_t m, std::size_t k,
+                                 std::size_t n, int cutoff) {
+    wm_report r{};
+    b200::check(wm_expected_costs(variant.c_str(), m, k, n, cutoff, &r));
+    return b200::to_report(variant, m, k, n, cutoff, r, nullptr);
+}
+}  // namespace models
+
+// Host-only plan: the exact CostReport the reference meter would produce.
+inline CostReport plan_only(const std::string& variant, std::size_t m, std::size_t k,
+                            std::size_t n, const MultiplyOptions& opt = {},
+                            std::uint32_t p = kDefaultModulus) {
+    wm_report r{};
+    b200::check(wm_plan_report(variant.c_str(), WM_FIELD_MODP, p, m, k, n, opt.alpha, opt.beta,
+                               opt.cutoff, 0, &r));
+    return b200::to_report(variant, m, k, n, opt.cutoff, r, nullptr);
+}
+
+inline const std::vector<std::string>& builtin_names() {
+    static const std::vector<std::string> n = {"std2", "acc3", "ip",   "ovl",  "ovl2",
+                                               "ovr",  "aclr", "accr", "acc2", "acr"};
+    return n;
+}
+
+inline bool variant_accumulates(const std::string& v) {
+    if (v == "ipmm" || v == "ipovmm" || v == "iprect" || v == "classic") return false;
+    if (v.rfind("blocked_acc_t", 0) == 0) return true;
+    for (const char* a : {"acc3", "aclr", "accr", "acc2", "acr"})
+        if (v == a) return true;
+    for (const auto& b : builtin_names())
+        if (v == b) return false;
+    throw unknown_schedule_error("unknown schedule: " + v);
+}
+
+}  // namespace winomem

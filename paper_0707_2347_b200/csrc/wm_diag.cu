@@ -1,0 +1,108 @@
+// Diagnostics used by scripts/microbench.py to calibrate the design (not on
+// the multiplication path): dependent-launch latency inside a CUDA graph with
+// and without programmatic dependent launch, and streaming bandwidth of a
+// one-CTA-per-SM copy (what one SM can pull from L2 / HBM).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/winomem_b200.h"
+
+namespace {
+
+__global__ void k_tiny(double* p, int pdl) {
+    if (pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    if (threadIdx.x == 0 && blockIdx.x == 0) p[0] += 1.0;
+    if (pdl) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+__global__ void k_stream(const double2* __restrict__ src, double2* __restrict__ dst,
+                         std::uint64_t n2, int write) {
+    double2 acc = make_double2(0, 0);
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n2;
+         i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        double2 v = __ldg(src + i);
+        if (write) dst[i] = v;
+        else {
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+    }
+    if (!write && acc.x == 12345.678) dst[0] = acc;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Average microseconds per kernel of `n` dependent single-CTA kernels replayed as
+// one CUDA graph (pdl=1: launched with programmatic stream serialization).
+int wm_diag_launch_latency(int n, int pdl, int blocks, double* us_per_kernel) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 12;
+    double* d = nullptr;
+    cudaMalloc(&d, 64);
+    cudaMemset(d, 0, 64);
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; i < n; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(blocks);
+        cfg.blockDim = dim3(128);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        cudaLaunchKernelEx(&cfg, k_tiny, d, pdl);
+    }
+    cudaStreamEndCapture(s, &g);
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) return 12;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaGraphLaunch(ge, s);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(e0, s);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *us_per_kernel = 1000.0 * ms / (reps * n);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(d);
+    cudaStreamDestroy(s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 12;
+}
+
+// GB/s of a grid of `blocks` x 256 threads streaming `bytes` (read-only when write=0).
+int wm_diag_stream(std::uint64_t bytes, int blocks, int write, int reps, double* gbs) {
+    cudaStream_t s;
+    cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+    double2 *a = nullptr, *b = nullptr;
+    if (cudaMalloc(&a, bytes) != cudaSuccess || cudaMalloc(&b, bytes) != cudaSuccess) return 12;
+    cudaMemset(a, 0, bytes);
+    const std::uint64_t n2 = bytes / 16;
+    k_stream<<<blocks, 256, 0, s>>>(a, b, n2, write);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) k_stream<<<blocks, 256, 0, s>>>(a, b, n2, write);
+    cudaEventRecord(e1, s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gbs = (write ? 2.0 : 1.0) * bytes * reps / (ms * 1e-3) / 1e9;
+    cudaFree(a);
+    cudaFree(b);
+    cudaStreamDestroy(s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 12;
+}
+
+}  // extern "C"
