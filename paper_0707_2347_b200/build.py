@@ -32,7 +32,8 @@ def _sources():
 
 
 def _headers():
-    return glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(INC, "*.h"))
+    return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+            glob.glob(os.path.join(INC, "*.h")))
 
 
 def _compile(src, hdr_mtime, verbose):
@@ -54,6 +55,8 @@ def _compile(src, hdr_mtime, verbose):
 
 def build(verbose=False, jobs=None):
     os.makedirs(OBJ, exist_ok=True)
+    from . import gen_fusion  # schedule-specific fused addition kernels
+    gen_fusion.main()
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 1)) as ex:
@@ -70,4 +73,6 @@ def build(verbose=False, jobs=None):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    sys.path.insert(0, os.path.dirname(HERE))
+    from paper_0707_2347_b200 import build as _b
+    print(_b.build(verbose="-v" in sys.argv))

@@ -55,6 +55,8 @@ __global__ void __launch_bounds__(128) k_leaf_dmma(const MulParams P) {
     const std::uint64_t row0 = static_cast<std::uint64_t>(blockIdx.y) * BM;
     const std::uint64_t col0 = static_cast<std::uint64_t>(blockIdx.x) * BN;
     const std::uint32_t M = P.m, N = P.n, K = P.k;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 
     auto load_tile = [&](int buf, std::uint32_t k0) {
 #pragma unroll
@@ -139,10 +141,17 @@ __global__ void __launch_bounds__(128) k_leaf_dmma(const MulParams P) {
 }  // namespace
 
 cudaError_t launch_leaf_dmma(const MulParams& P, bool real, cudaStream_t s) {
-    dim3 grid((P.n + BN - 1) / BN, (P.m + BM - 1) / BM);
-    if (real) k_leaf_dmma<true><<<grid, 128, 0, s>>>(P);
-    else k_leaf_dmma<false><<<grid, 128, 0, s>>>(P);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((P.n + BN - 1) / BN, (P.m + BM - 1) / BM);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (real) return cudaLaunchKernelEx(&cfg, k_leaf_dmma<true>, P);
+    return cudaLaunchKernelEx(&cfg, k_leaf_dmma<false>, P);
 }
 
 }  // namespace wm

@@ -1,0 +1,10 @@
+// Fused schedule-run kernels (generated bodies in wm_fused_gen.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "wm_fused_gen.cuh"
+
+namespace wm {
+cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s);
+}  // namespace wm

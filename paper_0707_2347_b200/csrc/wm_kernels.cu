@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "wm_device.h"
+#include "wm_fused.h"
 
 namespace wm {
 namespace {
@@ -48,8 +49,12 @@ __device__ __forceinline__ double apply(double a, double b, std::uint32_t mode, 
     return r >= p ? r - p : r;
 }
 
-template <bool REAL>
+template <bool REAL, int ILP>
 __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
+    // programmatic dependent launch: wait for the producer grid, then let the
+    // next kernel in the chain start its launch
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     int i = 0;
 #pragma unroll 1
     while (i + 1 < B.n && blockIdx.x >= B.it[i + 1].blk0) ++i;
@@ -63,12 +68,12 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
     if (t.vec == 2) {
         const std::uint32_t cv = t.cols >> 1;
         const std::uint64_t total = static_cast<std::uint64_t>(t.rows) * cv;
-        const std::uint64_t start = blk * (kAddThreads * kAddIlp) + threadIdx.x;
-        double2 av[kAddIlp], bv[kAddIlp];
-        std::uint64_t r[kAddIlp], c[kAddIlp];
-        bool ok[kAddIlp];
+        const std::uint64_t start = blk * (kAddThreads * ILP) + threadIdx.x;
+        double2 av[ILP], bv[ILP];
+        std::uint64_t r[ILP], c[ILP];
+        bool ok[ILP];
 #pragma unroll
-        for (int u = 0; u < kAddIlp; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const std::uint64_t idx = start + static_cast<std::uint64_t>(u) * kAddThreads;
             ok[u] = idx < total;
             r[u] = idx / cv;
@@ -79,7 +84,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
             }
         }
 #pragma unroll
-        for (int u = 0; u < kAddIlp; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             if (!ok[u]) continue;
             double2 o;
             o.x = apply<REAL>(av[u].x, two ? bv[u].x : 0.0, mode, sa, sb, p, pinv);
@@ -88,9 +93,9 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
         }
     } else {
         const std::uint64_t total = static_cast<std::uint64_t>(t.rows) * t.cols;
-        const std::uint64_t start = blk * (kAddThreads * kAddIlp) + threadIdx.x;
+        const std::uint64_t start = blk * (kAddThreads * ILP) + threadIdx.x;
 #pragma unroll
-        for (int u = 0; u < kAddIlp; ++u) {
+        for (int u = 0; u < ILP; ++u) {
             const std::uint64_t idx = start + static_cast<std::uint64_t>(u) * kAddThreads;
             if (idx >= total) break;
             const std::uint64_t rr = idx / t.cols, cc = idx - rr * t.cols;
@@ -99,6 +104,33 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
             t.d[rr * t.ldd + cc] = apply<REAL>(a, b, mode, sa, sb, p, pinv);
         }
     }
+}
+
+}  // namespace
+
+namespace fused {
+template <bool REAL>
+__device__ __forceinline__ double gop(std::uint32_t mode, double a, double b, double sa,
+                                      double sb, double p, double pinv) {
+    return apply<REAL>(a, b, mode, sa, sb, p, pinv);
+}
+}  // namespace fused
+
+namespace {
+
+// One fused run of a schedule's block additions: every thread owns one 16-B
+// position of the (identically shaped, pairwise disjoint) slot views and
+// executes the run's dataflow on registers -- each slot read once, written once.
+template <bool REAL>
+__global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams G) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint32_t cv = G.cols >> 1;
+    const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * cv;
+    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= total) return;
+    const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
+    fused::group_dispatch<REAL>(gid, G, r, c);
 }
 
 __global__ void k_u32_to_f64(double* __restrict__ dst, std::uint64_t ldd,
@@ -160,9 +192,48 @@ unsigned grid_for(std::uint64_t total) {
 }  // namespace
 
 cudaError_t launch_addsub(const AddBatch& b, bool real, unsigned blocks, cudaStream_t s) {
-    if (real) k_addsub<true><<<blocks, kAddThreads, 0, s>>>(b);
-    else k_addsub<false><<<blocks, kAddThreads, 0, s>>>(b);
-    return cudaGetLastError();
+    // blocks were counted at kAddIlp units per thread; small launches spread the
+    // same work over more CTAs (fewer units per thread) to fill the 148 SMs
+    int ilp = kAddIlp;
+    if (blocks * 4 <= 2 * 148) ilp = 1;
+    else if (blocks * 2 <= 2 * 148) ilp = 2;
+    AddBatch bb = b;
+    if (ilp != kAddIlp)
+        for (int i = 0; i < bb.n; ++i) bb.it[i].blk0 *= kAddIlp / ilp;
+    blocks *= kAddIlp / ilp;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kAddThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define WM_ADD_LAUNCH(I)                                                       \
+    if (ilp == I)                                                              \
+        return real ? cudaLaunchKernelEx(&cfg, k_addsub<true, I>, bb)          \
+                    : cudaLaunchKernelEx(&cfg, k_addsub<false, I>, bb);
+    WM_ADD_LAUNCH(1)
+    WM_ADD_LAUNCH(2)
+    WM_ADD_LAUNCH(4)
+#undef WM_ADD_LAUNCH
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s) {
+    const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * (G.cols / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((total + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G);
+    return cudaLaunchKernelEx(&cfg, k_group<false>, gid, G);
 }
 
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,

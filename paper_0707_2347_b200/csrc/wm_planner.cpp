@@ -356,6 +356,10 @@ struct Ctx {
     bool emit = true;
     std::vector<Op>* out = nullptr;
     const PlanOptions* opt = nullptr;
+    int* frame_counter = nullptr;
+    int frame = -1;
+    const char* sched = nullptr;
+    int row = 0;
 
     // ExecCtx::check_write (executor.hpp:40-49): region of the top-level call
     void check_write(const View& v, const char* what) const {
@@ -381,6 +385,9 @@ struct Ctx {
         op.sa = sa;
         op.sb = sb;
         op.depth = depth;
+        op.frame = frame;
+        op.sched = sched;
+        op.row = row;
         out->push_back(op);
     }
 };
@@ -505,6 +512,8 @@ void run_schedule(const Schedule& s, const View& A, const View& B, const View& C
         fail(E_DIMENSION, s.name + " is a plain product; beta must be 0");
 
     if (ctx.meter) ++ctx.meter->schedule_calls[s.name];
+    ctx.frame = ctx.frame_counter ? (*ctx.frame_counter)++ : -1;
+    ctx.sched = s.name.c_str();
     ctx.alpha_v = alpha;
     ctx.beta_v = beta;
     ctx.depth += 1;
@@ -550,7 +559,9 @@ void run_schedule(const Schedule& s, const View& A, const View& B, const View& C
         slot[id].vc = c;
     };
 
+    int rowno = 0;
     for (const auto& in : s.ins) {
+        ctx.row = ++rowno;
         if (in.kind == Instr::Product) {
             const View lv = operand(in.o0, "product"), rv = operand(in.o1, "product");
             if (lv.cols != rv.rows) fail(E_DIMENSION, "product inner dimensions disagree in " + s.name);
@@ -692,6 +703,8 @@ Plan plan_variant(const std::string& variant, Field f, std::uint64_t m, std::uin
     ctx.ws = &heap;
     ctx.out = &plan.ops;
     ctx.opt = &opt;
+    int frame_counter = 0;
+    ctx.frame_counter = &frame_counter;
     int t;
     std::string base;
 

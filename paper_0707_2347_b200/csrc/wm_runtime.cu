@@ -21,12 +21,14 @@
 
 #include "../../include/winomem_b200.h"
 #include "wm_device.h"
+#include "wm_fused.h"
 #include "wm_planner.h"
 
 namespace wm {
 cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s);      // wm_i8.cu
 cudaError_t launch_frame(const MulParams& P, bool real, cudaStream_t s);  // wm_frame.cu
 bool leaf_i8_supported(const MulParams& P);
+cudaError_t leaf_i8_init();
 bool frame_supported(const MulParams& P, bool real);
 bool frame_kernel_available();
 }  // namespace wm
@@ -51,11 +53,13 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 struct Step {
-    enum Kind : std::uint8_t { ADD, MUL, FRAME } kind;
+    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP } kind;
     AddBatch add;
     unsigned blocks = 0;
     MulParams mul;
     int leaf = 0;  // MUL: 0 dmma, 1 i8
+    int gid = -1;  // GROUP: fused schedule run
+    fused::GroupParams grp;
 };
 
 struct CachedPlan {
@@ -84,6 +88,7 @@ struct wm_ctx {
     bool batch_adds = true;
     int leaf_kernel = 0;  // 0 dmma, 1 i8, 2 auto
     int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames
+    bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
     // boundary staging
@@ -177,6 +182,71 @@ void init_batch(AddBatch& b, const Field& f) {
     b.pinv = 1.0 / static_cast<double>(f.p);
 }
 
+int find_group(const Op& op) {
+    if (op.frame < 0 || !op.sched) return -1;
+    for (int g = 0; g < fused::kNumGroups; ++g)
+        if (fused::kGroups[g].row0 == op.row && std::strcmp(fused::kGroups[g].sched, op.sched) == 0)
+            return g;
+    return -1;
+}
+
+// Bind the run of operations starting at ops[i] to fused group g: the rows must
+// be the group's rows of one frame instance, every slot must map to one view,
+// all views must share one shape, be pairwise disjoint and 16-B vectorisable.
+bool try_group(const Plan& plan, std::size_t i, int g, double* const base[4], Step& st) {
+    const fused::GroupDesc& G = fused::kGroups[g];
+    if (i + G.nins > plan.ops.size()) return false;
+    View slot[fused::kMaxSlots];
+    bool bound[fused::kMaxSlots] = {};
+    const Op& first = plan.ops[i];
+    auto bind = [&](int s, const View& v) {
+        if (!bound[s]) {
+            slot[s] = v;
+            bound[s] = true;
+            return true;
+        }
+        return slot[s].same_window(v);
+    };
+    for (int j = 0; j < G.nins; ++j) {
+        const Op& op = plan.ops[i + j];
+        if (op.kind != OP_ADDSUB && op.kind != OP_COPY) return false;
+        if (op.frame != first.frame || op.row != G.row0 + j) return false;
+        const int ds = G.ins[j][0], as = G.ins[j][1], bs = G.ins[j][2];
+        if ((bs < 0) != (op.kind == OP_COPY)) return false;
+        if (op.d.rows != first.d.rows || op.d.cols != first.d.cols) return false;
+        if (!bind(ds, op.d) || !bind(as, op.a) || (bs >= 0 && !bind(bs, op.b))) return false;
+    }
+    if (first.d.cols % 2) return false;
+    for (int a = 0; a < G.nslots; ++a) {
+        if (!bound[a]) return false;
+        for (int b = a + 1; b < G.nslots; ++b)
+            if (slot[a].phys_overlaps(slot[b])) return false;
+    }
+    const Field& f = plan.field;
+    std::memset(&st.grp, 0, sizeof(st.grp));
+    for (int a = 0; a < G.nslots; ++a) {
+        double* ptr = base[slot[a].region] + slot[a].off;
+        if (slot[a].ld % 2 || !aligned16(ptr)) return false;
+        st.grp.v[a] = ptr;
+        st.grp.ld[a] = slot[a].ld;
+    }
+    for (int j = 0; j < G.nins; ++j) {
+        const Op& op = plan.ops[i + j];
+        st.grp.mode[j] = op.kind == OP_ADDSUB
+                             ? modp_add_mode(f, op.sa, op.sb)
+                             : (f.is_one(op.sa) ? M_COPY : f.is_minus_one(op.sa) ? M_NEG : M_SCALE);
+        st.grp.sa[j] = f.real ? op.sa.d : static_cast<double>(op.sa.r);
+        st.grp.sb[j] = f.real ? op.sb.d : static_cast<double>(op.sb.r);
+    }
+    st.grp.rows = static_cast<std::uint32_t>(first.d.rows);
+    st.grp.cols = static_cast<std::uint32_t>(first.d.cols);
+    st.grp.p = static_cast<double>(f.p);
+    st.grp.pinv = 1.0 / static_cast<double>(f.p);
+    st.kind = Step::GROUP;
+    st.gid = g;
+    return true;
+}
+
 // Lower an operation list to launches.  Additions are merged into one launch
 // while they are pairwise independent (no write of one touches a read or
 // write of another) and contiguous in program order.
@@ -209,7 +279,18 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         return false;
     };
-    for (const Op& op : plan.ops) {
+    for (std::size_t oi = 0; oi < plan.ops.size(); ++oi) {
+        const Op& op = plan.ops[oi];
+        if ((op.kind == OP_ADDSUB || op.kind == OP_COPY) && ctx.fuse_adds) {
+            const int g = find_group(op);
+            Step gs{};
+            if (g >= 0 && try_group(plan, oi, g, base, gs)) {
+                flush();
+                steps.push_back(gs);
+                oi += fused::kGroups[g].nins - 1;
+                continue;
+            }
+        }
         if (op.kind == OP_ADDSUB || op.kind == OP_COPY) {
             if (!ctx.batch_adds || static_cast<int>(cur.size()) >= kMaxAddBatch || conflicts(op))
                 flush();
@@ -234,7 +315,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
 
 void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subset = 0) {
     for (const Step& s : steps) {
-        if (subset == 1 && s.kind != Step::ADD) continue;
+        if (subset == 1 && s.kind != Step::ADD && s.kind != Step::GROUP) continue;
         if (subset == 2 && s.kind != Step::MUL) continue;
         if (subset == 3 && s.kind != Step::FRAME) continue;
         switch (s.kind) {
@@ -244,6 +325,7 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
                 else WM_CUDA(launch_leaf_dmma(s.mul, real, st));
                 break;
             case Step::FRAME: WM_CUDA(launch_frame(s.mul, real, st)); break;
+            case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
         }
     }
 }
@@ -264,9 +346,19 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
     if (steps) r->n_launches = steps->size();
     r->add_bytes = (3 * plan.meter.add2_elems + 2 * plan.meter.copy_elems) * sizeof(double);
     r->leaf_flops = plan.meter.leaf_flops;
-    for (const auto& op : plan.ops) {
-        if (op.kind == OP_ADDSUB) r->add_bytes_issued += 3 * op.d.words() * sizeof(double);
-        if (op.kind == OP_COPY) r->add_bytes_issued += 2 * op.d.words() * sizeof(double);
+    if (steps) {
+        for (const Step& s : *steps) {
+            if (s.kind == Step::ADD)
+                for (int i = 0; i < s.add.n; ++i)
+                    r->add_bytes_issued += (s.add.it[i].mode <= M_GEN ? 3 : 2) *
+                                           static_cast<std::uint64_t>(s.add.it[i].rows) *
+                                           s.add.it[i].cols * sizeof(double);
+            if (s.kind == Step::GROUP) {
+                const fused::GroupDesc& G = fused::kGroups[s.gid];
+                r->add_bytes_issued += static_cast<std::uint64_t>(G.nload + G.nstore) *
+                                       s.grp.rows * s.grp.cols * sizeof(double);
+            }
+        }
     }
     std::ostringstream os;
     bool first = true;
@@ -307,7 +399,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -444,6 +536,7 @@ int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out)
         c->f.real = field == WM_FIELD_REAL64;
         c->f.p = field == WM_FIELD_REAL64 ? 65521u : p;
         WM_CUDA(cudaSetDevice(device));
+        WM_CUDA(leaf_i8_init());
         if (stream) {
             c->stream = static_cast<cudaStream_t>(stream);
         } else {
@@ -474,6 +567,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "batch_adds") ctx->batch_adds = value != 0;
         else if (k == "leaf_kernel") ctx->leaf_kernel = static_cast<int>(value);
         else if (k == "subset") ctx->subset = static_cast<int>(value);
+        else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
         else fail(E_INVALID, "unknown option " + k);
         ctx->cache.clear();
     });
@@ -487,6 +581,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "batch_adds") *value = ctx->batch_adds;
         else if (k == "leaf_kernel") *value = ctx->leaf_kernel;
         else if (k == "subset") *value = ctx->subset;
+        else if (k == "fuse_adds") *value = ctx->fuse_adds;
         else fail(E_INVALID, "unknown option " + k);
     });
 }
@@ -674,6 +769,48 @@ int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src) 
     return guard([&] {
         download(ctx, host, host_ld, src);
         WM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+// Diagnostics: average microseconds of `reps` back-to-back leaf products
+// C <- A*B (+C) captured as one graph (kernel: 0 DMMA, 1 tcgen05 int8).
+int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, int kernel,
+                      double* us) {
+    return guard([&] {
+        Op op{};
+        op.kind = OP_MUL;
+        op.d = raw_view(C);
+        op.a = raw_view(A);
+        op.b = raw_view(B);
+        op.sa = modp_scalar(ctx->f, 1);
+        op.sb = modp_scalar(ctx->f, 1);
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        MulParams P = make_mul(op, ctx->f, base);
+        if (kernel == 1 && !leaf_i8_supported(P)) fail(E_INVALID, "shape unsupported by i8 leaf");
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < reps; ++i) {
+            if (kernel == 1) launch_leaf_i8(P, ctx->stream);
+            else launch_leaf_dmma(P, ctx->f.real, ctx->stream);
+        }
+        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, ctx->stream);
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEventRecord(e1, ctx->stream);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *us = 1000.0 * ms / reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
     });
 }
 

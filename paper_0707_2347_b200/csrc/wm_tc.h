@@ -84,14 +84,22 @@ __device__ __forceinline__ void mbar_init(std::uint64_t* mbar, std::uint32_t cou
 __device__ __forceinline__ void mbar_fence_init() {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 }
-__device__ __forceinline__ void mbar_wait(std::uint64_t* mbar, std::uint32_t parity) {
+__device__ __forceinline__ bool mbar_try_wait(std::uint64_t* mbar, std::uint32_t parity) {
+    std::uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
-        "r"(parity)
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(mbar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// bounded wait: a lost arrival traps (a launch error) instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(std::uint64_t* mbar, std::uint32_t parity) {
+    std::uint32_t spins = 0;
+    while (!mbar_try_wait(mbar, parity))
+        if (++spins > (1u << 26)) __trap();
 }
 
 // 32 lanes x 32 bit, 16 consecutive columns per thread

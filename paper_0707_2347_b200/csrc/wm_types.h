@@ -122,6 +122,11 @@ struct Op {
     View d, a, b;
     Scalar sa, sb;
     int depth = 0;
+    // provenance: the schedule frame instance and 1-based row that emitted it
+    // (frame < 0: emitted by a driver outside any schedule frame)
+    int frame = -1;
+    const char* sched = nullptr;
+    int row = 0;
 };
 
 // CostMeter (meter.hpp:24-50)

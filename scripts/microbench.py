@@ -33,26 +33,22 @@ for blocks in (1, 8, 32, 148, 296, 592):
             out[f"stream_{'copy' if write else 'read'}_{size >> 20}MB_blocks{blocks}"] = v.value
 
 ctx = W.Context.get()
+L.wm_diag_time_leaf.argtypes = [C.c_void_p, _lib.wm_dmat, _lib.wm_dmat, _lib.wm_dmat, C.c_int,
+                                C.c_int, C.POINTER(C.c_double)]
 for leaf in (0, 1):
-    ctx.set_option("leaf_kernel", leaf)
     for n in (128, 256, 512, 1024, 2048, 4096):
+        # distinct buffers per rep would defeat L2; report the L2-warm figure
         A, B, Cm = W.Matrix(n, n), W.Matrix(n, n), W.Matrix(n, n)
         A.fill_random(1)
         B.fill_random(2)
-        W.classical_mul(Cm.view(), A.view(), B.view(), 1, 0)
         torch.cuda.synchronize()
-        reps = max(3, min(200, int(2e10 / (2 * n ** 3))))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ctx.enter()
-        e0.record(ctx.stream)
-        for _ in range(reps):
-            W.classical_mul(Cm.view(), A.view(), B.view(), 1, 0)
-        e1.record(ctx.stream)
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / 1e3 / reps
-        out[f"leaf{'_i8' if leaf else '_dmma'}_{n}_us"] = t * 1e6
-        out[f"leaf{'_i8' if leaf else '_dmma'}_{n}_tflops"] = 2 * n ** 3 / t / 1e12
-ctx.set_option("leaf_kernel", 0)
+        reps = max(3, min(500, int(4e10 / (2 * n ** 3))))
+        v = C.c_double()
+        rc = L.wm_diag_time_leaf(ctx.h, A.view().dmat(), B.view().dmat(), Cm.view().dmat(),
+                                 reps, leaf, C.byref(v))
+        t = v.value * 1e-6
+        out[f"leaf{'_i8' if leaf else '_dmma'}_{n}_us"] = v.value if rc == 0 else None
+        out[f"leaf{'_i8' if leaf else '_dmma'}_{n}_tflops"] = 2 * n ** 3 / t / 1e12 if rc == 0 else None
 print(json.dumps(out, indent=1))
 os.makedirs("gpurun_out", exist_ok=True)
 json.dump(out, open("gpurun_out/microbench.json", "w"), indent=1)

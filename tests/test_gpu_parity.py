@@ -186,3 +186,25 @@ def test_real64_winograd_frobenius(W, O):
         got = C.t.cpu().numpy()
         err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert err <= 1e-12 * 2 ** depth, (n, cutoff, err)
+
+
+@pytest.mark.parametrize("shape", [(128, 32, 64), (128, 128, 128), (256, 256, 256),
+                                   (384, 96, 192), (512, 1024, 128), (1024, 1024, 1024),
+                                   (128, 16384, 64)])
+def test_leaf_i8_vs_oracle(W, O, shape):
+    """tcgen05 int8-limb leaf kernel on tile-aligned shapes (incl. the long-K limb bound)."""
+    ctx = W.Context.get()
+    saved = ctx.get_option("leaf_kernel")
+    ctx.set_option("leaf_kernel", 1)
+    try:
+        m, k, n = shape
+        for (al, be) in [(1, 0), (1, 1), (3, 65520), (65520, 7)]:
+            A, B, C = _problem(W, m, k, n, m + k + n + al, True)
+            if k == 16384:  # worst case for the limb accumulators: all residues p-1
+                A.t.fill_(65520.0)
+                B.t.fill_(65520.0)
+            a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+            W.classical_mul(C.view(), A.view(), B.view(), al, be)
+            assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (shape, al, be)
+    finally:
+        ctx.set_option("leaf_kernel", saved)
