@@ -257,20 +257,41 @@ __global__ void __launch_bounds__(NT, 1) k_leaf_i8(const MulParams P) {
             }
         }
         cg::cluster_group cluster = cg::this_cluster();
-        cluster.sync();
         constexpr int ROWS = BM / SPLIT;
+        constexpr int ITER = ROWS * BN / NT;  // elements per thread, compile-time
+        // issue the C reads (beta != 0) before the cluster barrier so their
+        // latency overlaps it
+        double cin[ITER];
+        if (P.beta != 0) {
+#pragma unroll
+            for (int it = 0; it < ITER; ++it) {
+                const int e = it * NT + tid;
+                const int r = ks * ROWS + e / BN, c = e % BN;
+                cin[it] = P.C[(i0 + r) * P.ldc + j0 + c];
+            }
+        }
+        cluster.sync();
         const std::uint32_t* src[SPLIT];
 #pragma unroll
         for (int s = 0; s < SPLIT; ++s) src[s] = cluster.map_shared_rank(part, s);
-        for (int e = tid; e < ROWS * BN; e += NT) {
+        std::uint32_t pv[ITER][SPLIT];
+#pragma unroll
+        for (int it = 0; it < ITER; ++it) {
+            const int e = it * NT + tid;
+            const int r = ks * ROWS + e / BN, c = e % BN;
+#pragma unroll
+            for (int s = 0; s < SPLIT; ++s) pv[it][s] = src[s][r * PLD + c];
+        }
+#pragma unroll
+        for (int it = 0; it < ITER; ++it) {
+            const int e = it * NT + tid;
             const int r = ks * ROWS + e / BN, c = e % BN;
             double v = 0.0;
 #pragma unroll
-            for (int s = 0; s < SPLIT; ++s) v += static_cast<double>(src[s][r * PLD + c]);
+            for (int s = 0; s < SPLIT; ++s) v += static_cast<double>(pv[it][s]);
             v = reduce_modp(v, p, pinv) * al;
-            double* cp = P.C + (i0 + r) * P.ldc + j0 + c;
-            if (P.beta != 0) v = fma(be, *cp, v);
-            *cp = reduce_modp(v, p, pinv);
+            if (P.beta != 0) v = fma(be, cin[it], v);
+            P.C[(i0 + r) * P.ldc + j0 + c] = reduce_modp(v, p, pinv);
         }
         cluster.sync();
     }
@@ -330,6 +351,18 @@ cudaError_t leaf_i8_init() {
     if ((e = set_attr<32, 1>()) != cudaSuccess) return e;
     if ((e = set_attr<32, 2>()) != cudaSuccess) return e;
     return set_attr<32, 4>();
+}
+
+// measurement hook: force a (BN, SPLIT) configuration
+cudaError_t launch_leaf_i8_cfg(const MulParams& P, int bn, int split, cudaStream_t s) {
+    if (!leaf_i8_supported(P) || P.n % bn || P.k % (split * KC)) return cudaErrorInvalidValue;
+    if (bn == 64 && split == 1) return launch_cfg<64, 1>(P, s);
+    if (bn == 64 && split == 2) return launch_cfg<64, 2>(P, s);
+    if (bn == 64 && split == 4) return launch_cfg<64, 4>(P, s);
+    if (bn == 32 && split == 1) return launch_cfg<32, 1>(P, s);
+    if (bn == 32 && split == 2) return launch_cfg<32, 2>(P, s);
+    if (bn == 32 && split == 4) return launch_cfg<32, 4>(P, s);
+    return cudaErrorInvalidValue;
 }
 
 // Tile width and K split: aim for >= ~100 CTAs on the 148 SMs; a split needs

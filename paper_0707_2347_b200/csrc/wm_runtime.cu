@@ -29,6 +29,7 @@ cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s);      // wm_i8.cu
 cudaError_t launch_frame(const MulParams& P, bool real, cudaStream_t s);  // wm_frame.cu
 bool leaf_i8_supported(const MulParams& P);
 cudaError_t leaf_i8_init();
+cudaError_t launch_leaf_i8_cfg(const MulParams& P, int bn, int split, cudaStream_t s);
 bool frame_supported(const MulParams& P, bool real);
 bool frame_kernel_available();
 }  // namespace wm
@@ -776,6 +777,7 @@ int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src) 
 // C <- A*B (+C) captured as one graph (kernel: 0 DMMA, 1 tcgen05 int8).
 int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, int kernel,
                       double* us) {
+    // kernel: 0 DMMA, 1 int8 (auto config), 100*bn + split: int8 forced config
     return guard([&] {
         Op op{};
         op.kind = OP_MUL;
@@ -786,13 +788,21 @@ int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, in
         op.sb = modp_scalar(ctx->f, 1);
         double* base[4] = {nullptr, nullptr, nullptr, nullptr};
         MulParams P = make_mul(op, ctx->f, base);
-        if (kernel == 1 && !leaf_i8_supported(P)) fail(E_INVALID, "shape unsupported by i8 leaf");
+        if (kernel >= 1 && !leaf_i8_supported(P)) fail(E_INVALID, "shape unsupported by i8 leaf");
         cudaGraph_t g;
         cudaGraphExec_t ge;
         WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         for (int i = 0; i < reps; ++i) {
-            if (kernel == 1) launch_leaf_i8(P, ctx->stream);
-            else launch_leaf_dmma(P, ctx->f.real, ctx->stream);
+            cudaError_t e;
+            if (kernel == 1) e = launch_leaf_i8(P, ctx->stream);
+            else if (kernel > 1) e = launch_leaf_i8_cfg(P, kernel / 100, kernel % 100, ctx->stream);
+            else e = launch_leaf_dmma(P, ctx->f.real, ctx->stream);
+            if (e != cudaSuccess) {
+                cudaGraph_t g2;
+                cudaStreamEndCapture(ctx->stream, &g2);
+                if (g2) cudaGraphDestroy(g2);
+                fail(E_INVALID, "leaf config rejected");
+            }
         }
         WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
         WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
