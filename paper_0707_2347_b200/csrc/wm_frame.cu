@@ -1,7 +1,200 @@
-// placeholder, replaced by the fused frame kernel
-#include "wm_device.h"
+// Fused leaf frames.  A Winograd frame whose seven products are classical
+// leaves (the bottom level of every recursion) runs as three launches instead
+// of ~15-24 additions and 7 leaf products issued one after another:
+//
+//  prep  S1 = A21+A22, S2 = S1-A11, S3 = A11-A21, S4 = A12-S2 and
+//        T1 = B12-B11, T2 = B22-T1, T3 = B22-B12, T4 = T2-B21 (Table 1) as uint16
+//        residue planes; for accumulating frames beta*C_in is packed as four
+//        uint16 per position into the C11 slots;
+//  gemm  the seven products P1 = A11 B11, P2 = A12 B21, P3 = S4 B22,
+//        P4 = A22 T4, P5 = S1 T1, P6 = S2 T2, P7 = S3 T3 in ONE int8-limb GEMM
+//        launch (wm_i8.cu, blockIdx.z = product), written as uint16 planes;
+//  comb  U1 = P1+P2, U2 = P1+P6, U3 = U2+P7, U4 = U2+P5, U5 = U4+P3,
+//        U6 = U3-P4, U7 = U3+P5 and C_ij = alpha*U + beta*C_in, float64 out.
+//
+// No memory beyond the schedule's own: a "host" is a c x c float64 block whose
+// rows each hold four uint16 plane rows (8c bytes).  S/T planes live in C
+// blocks that are dead until the combine (C11, C12 for plain frames; C12, C21
+// once beta*C_in is packed into C11), the P planes in the frame's temporaries
+// or -- for ip / ovl / ovr, which have fewer -- in the A21 / B12 blocks their
+// contract lets them overwrite.  Every prep / comb thread owns a fixed set of
+// float64 slots (it reads them before it overwrites them), so the in-place
+// packing is race-free.
+#include <cstdint>
+
+#include "wm_frame.h"
+
 namespace wm {
-bool frame_supported(const MulParams&, bool) { return false; }
-bool frame_kernel_available() { return false; }
-cudaError_t launch_frame(const MulParams&, bool, cudaStream_t) { return cudaErrorNotSupported; }
+namespace {
+
+__device__ __forceinline__ double rmod(double v, double p, double pinv) {
+    const double q = floor(v * pinv);
+    double r = fma(-q, p, v);
+    r = r < 0.0 ? r + p : r;
+    return r >= p ? r - p : r;
+}
+__device__ __forceinline__ double addm(double a, double b, double p) {
+    const double v = a + b;
+    return v >= p ? v - p : v;
+}
+__device__ __forceinline__ double subm(double a, double b, double p) {
+    const double v = a - b;
+    return v < 0.0 ? v + p : v;
+}
+
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
+}
+
+__device__ __forceinline__ uint2 pack(double a, double b, double c, double d) {
+    return make_uint2(static_cast<std::uint32_t>(a) | (static_cast<std::uint32_t>(b) << 16),
+                      static_cast<std::uint32_t>(c) | (static_cast<std::uint32_t>(d) << 16));
+}
+
+// thread (r, q), q < c/4: plane columns j = 4q..4q+3, owned float64 slots
+// (r, q + k c/4) for k = 0..3 of every host / C block.
+__global__ void __launch_bounds__(256) k_frame_prep(const FramePrepParams P) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint32_t c4 = P.c / 4;
+    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<std::uint64_t>(P.c) * c4) return;
+    const std::uint64_t r = idx / c4, q = idx - r * c4, j = 4 * q;
+    const double p = P.pd, pinv = P.pinv;
+
+    double a11[4], a12[4], a21[4], a22[4], b11[4], b12[4], b21[4], b22[4];
+    ld4(P.A.q[0] + r * P.A.ld + j, a11);
+    ld4(P.A.q[1] + r * P.A.ld + j, a12);
+    ld4(P.A.q[2] + r * P.A.ld + j, a21);
+    ld4(P.A.q[3] + r * P.A.ld + j, a22);
+    ld4(P.B.q[0] + r * P.B.ld + j, b11);
+    ld4(P.B.q[1] + r * P.B.ld + j, b12);
+    ld4(P.B.q[2] + r * P.B.ld + j, b21);
+    ld4(P.B.q[3] + r * P.B.ld + j, b22);
+    // beta * C_in of the four owned slots, read before any host slot is written
+    double cin[4][4];
+    if (P.beta != 0) {
+        const double be = static_cast<double>(P.beta);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int qd = 0; qd < 4; ++qd)
+                cin[k][qd] = rmod(be * P.C.q[qd][r * P.C.ld + q + k * c4], p, pinv);
+    }
+    double s[4][4], t[4][4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const double s1 = addm(a21[e], a22[e], p), s2 = subm(s1, a11[e], p);
+        s[0][e] = s1;
+        s[1][e] = s2;
+        s[2][e] = subm(a11[e], a21[e], p);
+        s[3][e] = subm(a12[e], s2, p);
+        const double t1 = subm(b12[e], b11[e], p), t2 = subm(b22[e], t1, p);
+        t[0][e] = t1;
+        t[1][e] = t2;
+        t[2][e] = subm(b22[e], b12[e], p);
+        t[3][e] = subm(t2, b21[e], p);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        *reinterpret_cast<uint2*>(P.s_host + r * 4 * P.s_ld + 4 * (q + k * c4)) =
+            pack(s[k][0], s[k][1], s[k][2], s[k][3]);
+        *reinterpret_cast<uint2*>(P.t_host + r * 4 * P.t_ld + 4 * (q + k * c4)) =
+            pack(t[k][0], t[k][1], t[k][2], t[k][3]);
+    }
+    if (P.beta != 0) {
+        std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            *reinterpret_cast<uint2*>(c11 + 4 * (r * P.C.ld + q + k * c4)) =
+                pack(cin[k][0], cin[k][1], cin[k][2], cin[k][3]);
+    }
+}
+
+// thread (r, 4 consecutive columns j..j+3) of the quadrant
+__global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint32_t c4 = P.c / 4;
+    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    if (idx >= static_cast<std::uint64_t>(P.c) * c4) return;
+    const std::uint64_t r = idx / c4, j = 4 * (idx - r * c4);
+    const double p = P.pd, pinv = P.pinv;
+    double pv[7][4];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const uint2 w = *reinterpret_cast<const uint2*>(P.P[k] + r * P.pld[k] + j);
+        pv[k][0] = static_cast<double>(w.x & 0xFFFFu);
+        pv[k][1] = static_cast<double>(w.x >> 16);
+        pv[k][2] = static_cast<double>(w.y & 0xFFFFu);
+        pv[k][3] = static_cast<double>(w.y >> 16);
+    }
+    double cin[4][4];  // [col e][quadrant]
+    if (P.beta != 0) {
+        const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const uint2 w =
+                *reinterpret_cast<const uint2*>(c11 + 4 * (r * P.C.ld + j + e));
+            cin[e][0] = static_cast<double>(w.x & 0xFFFFu);
+            cin[e][1] = static_cast<double>(w.x >> 16);
+            cin[e][2] = static_cast<double>(w.y & 0xFFFFu);
+            cin[e][3] = static_cast<double>(w.y >> 16);
+        }
+    }
+    const double al = static_cast<double>(P.alpha);
+    double out[4][4];  // [quadrant][col]
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const double p1 = pv[0][e], p2 = pv[1][e], p3 = pv[2][e], p4 = pv[3][e],
+                     p5 = pv[4][e], p6 = pv[5][e], p7 = pv[6][e];
+        const double u2 = p1 + p6;
+        const double u3 = u2 + p7;
+        const double u[4] = {p1 + p2, u2 + p5 + p3, u3 + (p - p4), u3 + p5};  // < 4p
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            double v = rmod(u[qd], p, pinv) * al;
+            if (P.beta != 0) v += cin[e][qd];
+            out[qd][e] = rmod(v, p, pinv);
+        }
+    }
+#pragma unroll
+    for (int qd = 0; qd < 4; ++qd) {
+        double* dst = P.C.q[qd] + r * P.C.ld + j;
+        *reinterpret_cast<double2*>(dst) = make_double2(out[qd][0], out[qd][1]);
+        *reinterpret_cast<double2*>(dst + 2) = make_double2(out[qd][2], out[qd][3]);
+    }
+}
+
+template <class K, class Prm>
+cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>((threads + 255) / 256));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+}  // namespace
+
+cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
+    return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 4), s);
+}
+
+cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s) {
+    return launch_pdl(k_frame_comb, P, static_cast<std::uint64_t>(P.c) * (P.c / 4), s);
+}
+
+bool frame_kernel_available() { return true; }
+
 }  // namespace wm

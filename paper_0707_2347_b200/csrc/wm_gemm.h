@@ -1,0 +1,32 @@
+// Generalised exact int8-limb GEMM launch parameters (wm_i8.cu): several
+// independent products of one shape per launch, float64 or uint16 residue
+// operands, float64 (alpha/beta) or uint16 outputs.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace wm {
+
+constexpr int kMaxProducts = 7;
+
+struct GemmSrc {
+    const void* p;
+    std::uint64_t ld;   // in elements
+    std::uint32_t fmt;  // 0 float64 residues, 1 uint16 residues
+};
+
+struct GemmParams {
+    GemmSrc a[kMaxProducts], b[kMaxProducts], c[kMaxProducts];
+    std::uint32_t m, n, k;   // shape of every product
+    std::uint32_t nprod;     // products in this launch
+    std::uint32_t tiles_m;   // m / 128
+    std::uint32_t alpha, beta;  // float64 outputs only
+    double pd, pinv;
+};
+
+bool gemm_i8_supported(const GemmParams& P);
+cudaError_t launch_gemm_i8(const GemmParams& P, cudaStream_t s);
+
+}  // namespace wm

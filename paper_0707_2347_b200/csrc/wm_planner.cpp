@@ -357,6 +357,7 @@ struct Ctx {
     std::vector<Op>* out = nullptr;
     const PlanOptions* opt = nullptr;
     int* frame_counter = nullptr;
+    std::vector<View>* capture_temps = nullptr;  // dry run of a fused frame
     int frame = -1;
     const char* sched = nullptr;
     int row = 0;
@@ -457,23 +458,30 @@ void run_schedule(const Schedule& s, const View& A, const View& B, const View& C
 void peel_multiply(const View& A, const View& B, const View& C, Scalar alpha, Scalar beta,
                    const std::string& base, Ctx ctx);
 
-// Can this frame run as one fused OP_FRAME?  Every product must be a classical
-// leaf, the operands must not alias the output (the kernel tiles C), and the
-// leaf block must suit the kernel's tiling.
+// Can this frame run fused (wm_frame.cu)?  Every product must be a classical
+// leaf, the frame square with the leaf size a multiple of the GEMM tile, the
+// output disjoint from the operands (the kernels tile C), the field Z/pZ, and
+// the frame must own two c x c blocks to host the seven product planes: two of
+// its temporaries, or -- when its contract lets it overwrite A / B -- the
+// A21 / B12 blocks (whose raw values the fused products never read).
 bool frame_fusable(const std::string& variant, const View& A, const View& B, const View& C,
                    const Ctx& ctx) {
-    if (!ctx.opt || !ctx.opt->fuse_frames || !ctx.emit) return false;
+    if (!ctx.opt || !ctx.opt->fuse_frames || !ctx.emit || ctx.f.real) return false;
     if (ctx.peel || !is_builtin(variant)) return false;
     const std::uint64_t m = A.rows, k = A.cols, n = B.cols;
-    if (m % 2 || k % 2 || n % 2) return false;
-    const std::uint64_t c = static_cast<std::uint64_t>(ctx.cutoff);
-    if (std::min({m, k, n}) / 2 > c) return false;  // children recurse
-    const std::uint64_t al = static_cast<std::uint64_t>(ctx.opt->frame_align);
-    if ((m / 2) % al || (k / 2) % al || (n / 2) % al) return false;
-    if (std::max({m, k, n}) / 2 > static_cast<std::uint64_t>(ctx.opt->frame_max_leaf))
-        return false;
+    if (m != k || k != n || m % 2) return false;
+    const std::uint64_t c = m / 2;
+    if (c > static_cast<std::uint64_t>(ctx.cutoff)) return false;  // children recurse
+    if (c % static_cast<std::uint64_t>(ctx.opt->frame_align)) return false;
+    if (c > static_cast<std::uint64_t>(ctx.opt->frame_max_leaf)) return false;
     if (C.phys_overlaps(A) || C.phys_overlaps(B)) return false;
-    return true;
+    const Schedule& s = builtin(variant);
+    int big = 0;
+    for (const auto& t : s.temps)
+        big += eval_dim(t.rows, m, k, n) >= c && eval_dim(t.cols, m, k, n) >= c;
+    const bool ovA = s.contract == Contract::OverwriteA || s.contract == Contract::OverwriteBoth;
+    const bool ovB = s.contract == Contract::OverwriteB || s.contract == Contract::OverwriteBoth;
+    return big + (ovA ? 1 : 0) + (ovB ? 1 : 0) >= 2;
 }
 
 // multiply_into (executor.hpp:71-80)
@@ -486,15 +494,40 @@ void multiply_into(const std::string& variant, const View& A, const View& B, con
         return;
     }
     if (frame_fusable(variant, A, B, C, ctx)) {
-        // meter and validate the frame exactly as the reference walks it, then
-        // issue it as one fused kernel
+        // meter and validate the frame exactly as the reference walks it
+        // (capturing its temporaries), then issue it fused
+        std::vector<View> temps;
         Ctx dry = ctx;
         dry.emit = false;
+        dry.capture_temps = &temps;
         run_schedule(builtin(variant), A, B, C, alpha, beta, dry);
         ctx.check_write(C, "frame");
-        Ctx e = ctx;
-        e.depth = ctx.depth + 1;
-        e.emit_op(OP_FRAME, C, A, B, alpha, beta);
+        const Schedule& s = builtin(variant);
+        const std::uint64_t c = A.rows / 2;
+        std::vector<View> hosts;
+        for (const View& t : temps)
+            if (t.rows >= c && t.cols >= c && hosts.size() < 2) hosts.push_back(t.window(0, 0, c, c));
+        const bool ovA = s.contract == Contract::OverwriteA || s.contract == Contract::OverwriteBoth;
+        const bool ovB = s.contract == Contract::OverwriteB || s.contract == Contract::OverwriteBoth;
+        if (hosts.size() < 2 && ovA) hosts.push_back(quad_split(A)[2]);
+        if (hosts.size() < 2 && ovB) hosts.push_back(quad_split(B)[1]);
+        if (hosts.size() < 2) fail(E_INVALID, "fused frame without plane hosts");
+        if (ctx.emit && ctx.out) {
+            Op op;
+            op.kind = OP_FRAME;
+            op.d = C;
+            op.a = A;
+            op.b = B;
+            op.sa = alpha;
+            op.sb = beta;
+            op.depth = ctx.depth + 1;
+            op.frame = ctx.frame;
+            op.sched = s.name.c_str();
+            op.row = ctx.row;
+            op.h0 = hosts[0];
+            op.h1 = hosts[1];
+            ctx.out->push_back(op);
+        }
         return;
     }
     run_schedule(builtin(variant), A, B, C, alpha, beta, ctx);
@@ -534,7 +567,9 @@ void run_schedule(const Schedule& s, const View& A, const View& B, const View& C
     for (const auto& t : s.temps) {
         const std::uint64_t r = eval_dim(t.rows, m, k, n), c = eval_dim(t.cols, m, k, n);
         slot[t.slot] = {ctx.ws->acquire(r, c, ctx.depth, slot_name(t.slot)), 0, 0, false, false};
+        if (ctx.capture_temps) ctx.capture_temps->push_back(slot[t.slot].buf);
     }
+    ctx.capture_temps = nullptr;  // only the fused frame's own temporaries
 
     auto operand = [&](Slot id, const char* what) -> View {
         Bound& b = slot[id];

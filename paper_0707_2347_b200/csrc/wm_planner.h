@@ -27,8 +27,8 @@ struct PlanOptions {
     // is still walked instruction by instruction and its temporaries are still
     // acquired in the arena.
     bool fuse_frames = false;
-    // The FRAME kernel supports leaf sizes that are multiples of this.
-    int frame_align = 64;
+    // The FRAME kernels support leaf sizes that are multiples of this.
+    int frame_align = 128;
     int frame_max_leaf = 1 << 20;
 };
 

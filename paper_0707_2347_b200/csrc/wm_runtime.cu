@@ -21,16 +21,16 @@
 
 #include "../../include/winomem_b200.h"
 #include "wm_device.h"
+#include "wm_frame.h"
 #include "wm_fused.h"
+#include "wm_gemm.h"
 #include "wm_planner.h"
 
 namespace wm {
 cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s);      // wm_i8.cu
-cudaError_t launch_frame(const MulParams& P, bool real, cudaStream_t s);  // wm_frame.cu
 bool leaf_i8_supported(const MulParams& P);
 cudaError_t leaf_i8_init();
 cudaError_t launch_leaf_i8_cfg(const MulParams& P, int bn, int split, cudaStream_t s);
-bool frame_supported(const MulParams& P, bool real);
 bool frame_kernel_available();
 }  // namespace wm
 
@@ -54,13 +54,16 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 struct Step {
-    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP } kind;
+    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB } kind;
     AddBatch add;
     unsigned blocks = 0;
     MulParams mul;
     int leaf = 0;  // MUL: 0 dmma, 1 i8
     int gid = -1;  // GROUP: fused schedule run
     fused::GroupParams grp;
+    FramePrepParams fprep;  // fused leaf frame, three launches
+    GemmParams fgemm;
+    FrameCombParams fcomb;
 };
 
 struct CachedPlan {
@@ -248,6 +251,86 @@ bool try_group(const Plan& plan, std::size_t i, int g, double* const base[4], St
     return true;
 }
 
+// A fused leaf frame -> prep / seven-product GEMM / combine launches.
+void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps) {
+    const std::uint64_t c = op.a.rows / 2;
+    auto ptr = [&](const View& v) { return base[v.region] + v.off; };
+    const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
+    const bool acc = !f.is_zero(op.sb);
+    const View& sh = acc ? cq[1] : cq[0];  // S planes host
+    const View& th = acc ? cq[2] : cq[1];  // T planes host
+    auto plane = [&](const View& host, int q) {
+        GemmSrc g;
+        g.p = reinterpret_cast<std::uint16_t*>(ptr(host)) + q * c;
+        g.ld = 4 * host.ld;
+        g.fmt = 1;
+        return g;
+    };
+    auto f64 = [&](const View& v) {
+        GemmSrc g;
+        g.p = ptr(v);
+        g.ld = v.ld;
+        g.fmt = 0;
+        return g;
+    };
+    const double pd = static_cast<double>(f.p), pinv = 1.0 / static_cast<double>(f.p);
+    Step p{};
+    p.kind = Step::FPREP;
+    for (int i = 0; i < 4; ++i) {
+        p.fprep.A.q[i] = ptr(aq[i]);
+        p.fprep.B.q[i] = ptr(bq[i]);
+        p.fprep.C.q[i] = ptr(cq[i]);
+    }
+    p.fprep.A.ld = op.a.ld;
+    p.fprep.B.ld = op.b.ld;
+    p.fprep.C.ld = op.d.ld;
+    p.fprep.s_host = reinterpret_cast<std::uint16_t*>(ptr(sh));
+    p.fprep.s_ld = sh.ld;
+    p.fprep.t_host = reinterpret_cast<std::uint16_t*>(ptr(th));
+    p.fprep.t_ld = th.ld;
+    p.fprep.c = static_cast<std::uint32_t>(c);
+    p.fprep.beta = op.sb.r;
+    p.fprep.pd = pd;
+    p.fprep.pinv = pinv;
+    steps.push_back(p);
+
+    Step g{};
+    g.kind = Step::FGEMM;
+    GemmParams& G = g.fgemm;
+    // P1 = A11 B11, P2 = A12 B21, P3 = S4 B22, P4 = A22 T4, P5 = S1 T1, P6 = S2 T2, P7 = S3 T3
+    G.a[0] = f64(aq[0]);   G.b[0] = f64(bq[0]);
+    G.a[1] = f64(aq[1]);   G.b[1] = f64(bq[2]);
+    G.a[2] = plane(sh, 3); G.b[2] = f64(bq[3]);
+    G.a[3] = f64(aq[3]);   G.b[3] = plane(th, 3);
+    G.a[4] = plane(sh, 0); G.b[4] = plane(th, 0);
+    G.a[5] = plane(sh, 1); G.b[5] = plane(th, 1);
+    G.a[6] = plane(sh, 2); G.b[6] = plane(th, 2);
+    for (int k = 0; k < 7; ++k) G.c[k] = k < 4 ? plane(op.h0, k) : plane(op.h1, k - 4);
+    G.m = G.n = G.k = static_cast<std::uint32_t>(c);
+    G.nprod = 7;
+    G.tiles_m = static_cast<std::uint32_t>(c / 128);
+    G.alpha = 1;
+    G.beta = 0;
+    G.pd = pd;
+    G.pinv = pinv;
+    steps.push_back(g);
+
+    Step cb{};
+    cb.kind = Step::FCOMB;
+    for (int k = 0; k < 7; ++k) {
+        cb.fcomb.P[k] = static_cast<const std::uint16_t*>(G.c[k].p);
+        cb.fcomb.pld[k] = G.c[k].ld;
+    }
+    for (int i = 0; i < 4; ++i) cb.fcomb.C.q[i] = ptr(cq[i]);
+    cb.fcomb.C.ld = op.d.ld;
+    cb.fcomb.c = static_cast<std::uint32_t>(c);
+    cb.fcomb.alpha = op.sa.r;
+    cb.fcomb.beta = op.sb.r;
+    cb.fcomb.pd = pd;
+    cb.fcomb.pinv = pinv;
+    steps.push_back(cb);
+}
+
 // Lower an operation list to launches.  Additions are merged into one launch
 // while they are pairwise independent (no write of one touches a read or
 // write of another) and contiguous in program order.
@@ -299,11 +382,13 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             continue;
         }
         flush();
+        if (op.kind == OP_FRAME) {
+            lower_frame(op, f, base, steps);
+            continue;
+        }
         Step s{};
         s.mul = make_mul(op, f, base);
-        if (op.kind == OP_FRAME) {
-            s.kind = Step::FRAME;
-        } else {
+        {
             s.kind = Step::MUL;
             const bool i8ok = !f.real && leaf_i8_supported(s.mul);
             s.leaf = (ctx.leaf_kernel == 1 || ctx.leaf_kernel == 2) && i8ok ? 1 : 0;
@@ -318,15 +403,19 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
     for (const Step& s : steps) {
         if (subset == 1 && s.kind != Step::ADD && s.kind != Step::GROUP) continue;
         if (subset == 2 && s.kind != Step::MUL) continue;
-        if (subset == 3 && s.kind != Step::FRAME) continue;
+        if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB)
+            continue;
         switch (s.kind) {
             case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
             case Step::MUL:
                 if (s.leaf == 1) WM_CUDA(launch_leaf_i8(s.mul, st));
                 else WM_CUDA(launch_leaf_dmma(s.mul, real, st));
                 break;
-            case Step::FRAME: WM_CUDA(launch_frame(s.mul, real, st)); break;
+            case Step::FRAME: break;
             case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
+            case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
+            case Step::FGEMM: WM_CUDA(launch_gemm_i8(s.fgemm, st)); break;
+            case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
         }
     }
 }

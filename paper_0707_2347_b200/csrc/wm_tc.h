@@ -102,6 +102,24 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* mbar, std::uint32_t par
         if (++spins > (1u << 26)) __trap();
 }
 
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* mbar, std::uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)),
+                 "r"(bytes)
+                 : "memory");
+}
+// bulk global -> shared copy completing `bytes` of transaction on mbar (size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32_t bytes,
+                                         std::uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns per thread
 __device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t (&r)[16]) {
     asm volatile(

@@ -127,6 +127,8 @@ struct Op {
     int frame = -1;
     const char* sched = nullptr;
     int row = 0;
+    // OP_FRAME: the two c x c blocks that host the seven product planes
+    View h0, h1;
 };
 
 // CostMeter (meter.hpp:24-50)

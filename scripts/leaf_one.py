@@ -10,7 +10,7 @@ import paper_0707_2347_b200 as W  # noqa: E402
 from paper_0707_2347_b200 import _lib  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 256
-kern = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+kern = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # 1 auto, 100*bn+split forced
 L = _lib.lib()
 L.wm_diag_time_leaf.argtypes = [C.c_void_p, _lib.wm_dmat, _lib.wm_dmat, _lib.wm_dmat, C.c_int,
                                 C.c_int, C.POINTER(C.c_double)]

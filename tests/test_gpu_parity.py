@@ -140,10 +140,14 @@ def test_midsize_vs_oracle(W, O, v, options):
 CFG = json.load(open(os.path.join(GOLD, "config_hashes.json")))
 
 
+@pytest.mark.parametrize("fused", [0, 1], ids=["unfused", "fused"])
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
-def test_config_full_size_hash(W, name):
+def test_config_full_size_hash(W, name, fused):
     if name not in CFG:
         pytest.skip("hash not generated")
+    ctx = W.Context.get()
+    ctx.set_option("fuse_frames", fused)
+    ctx.set_option("leaf_kernel", 2)
     c = CFG[name]
     want = c["appendix_a"]
     A, B, C = _problem(W, c["m"], c["k"], c["n"], c["seed"], bool(c["beta"]))
