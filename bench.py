@@ -305,6 +305,8 @@ def main():
     t_add = subset_time(1)
     t_leaf = subset_time(2)
     t_frame = subset_time(3) if rep.fused_frames else 0.0
+    frame_parts = ({"prep": subset_time(4), "gemm": subset_time(5), "comb": subset_time(6)}
+                   if rep.fused_frames else {})
     hbm, hbm_src = peaks()
     add_issued = rep.add_bytes_issued
     comps = {"additions": t_add, "leaf_products": t_leaf, "fused_frames": t_frame}
@@ -347,6 +349,7 @@ def main():
                                                       cfg["cutoff"]).peak_extra_words,
         "parity": parity,
         "breakdown_s": comps,
+        "frame_breakdown_s": frame_parts,
         "roofline": roof,
         "gpu_launches": rep.n_launches * args.steps,
         "launches_per_step": rep.n_launches,

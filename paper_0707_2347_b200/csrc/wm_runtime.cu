@@ -87,11 +87,11 @@ struct wm_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     // options
-    bool fuse_frames = false;
+    bool fuse_frames = true;
     bool graphs = true;
     bool batch_adds = true;
-    int leaf_kernel = 0;  // 0 dmma, 1 i8, 2 auto
-    int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames
+    int leaf_kernel = 2;  // 0 dmma, 1 i8, 2 auto (i8 where the tiles fit, else dmma)
+    int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames, 4/5/6 frame prep/gemm/comb
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
@@ -405,6 +405,9 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
         if (subset == 2 && s.kind != Step::MUL) continue;
         if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB)
             continue;
+        if (subset == 4 && s.kind != Step::FPREP) continue;
+        if (subset == 5 && s.kind != Step::FGEMM) continue;
+        if (subset == 6 && s.kind != Step::FCOMB) continue;
         switch (s.kind) {
             case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
             case Step::MUL:

@@ -41,13 +41,13 @@ def golden():
     return json.load(open(os.path.join(GOLD, "small_cases.json")))["cases"]
 
 
-@pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0), dict(fuse_frames=1),
-                        dict(leaf_kernel=1), dict(leaf_kernel=1, fuse_frames=1)],
-                ids=["default", "nograph", "fused", "i8", "i8-fused"])
+@pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
+                        dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0)],
+                ids=["default", "nograph", "unfused-i8", "unfused-dmma"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
-                                              "leaf_kernel")}
+                                              "leaf_kernel", "fuse_adds")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
