@@ -5,6 +5,7 @@
 
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace wm {
@@ -26,7 +27,18 @@ struct GemmParams {
     double pd, pinv;
 };
 
+// TMA operand maps (one pair per product), encoded on the host at lowering time
+struct TmaMaps {
+    CUtensorMap a[kMaxProducts], b[kMaxProducts];
+};
+
 bool gemm_i8_supported(const GemmParams& P);
-cudaError_t launch_gemm_i8(const GemmParams& P, cudaStream_t s);
+// (BN, K split) for a product set: aim for >= ~100 CTAs on the 148 SMs
+void gemm_choose(const GemmParams& P, int* bn, int* split);
+cudaError_t launch_gemm_i8(const GemmParams& P, cudaStream_t s);             // cp.async engine
+cudaError_t gemm_tma_init();
+bool gemm_tma_encode(const GemmParams& P, int bn, TmaMaps& M);
+cudaError_t launch_gemm_tma(const GemmParams& P, const TmaMaps& M, int bn, int split,
+                            cudaStream_t s);                                  // TMA engine
 
 }  // namespace wm

@@ -462,26 +462,35 @@ cudaError_t leaf_i8_init() {
 
 // Tile width and K split: aim for >= ~100 CTAs on the 148 SMs; a split needs
 // every slice to be a whole number of 32-wide chunks.
-cudaError_t launch_gemm_i8(const GemmParams& P, cudaStream_t s) {
-    if (!gemm_i8_supported(P)) return cudaErrorInvalidValue;
+void gemm_choose(const GemmParams& P, int* bn, int* split) {
     const std::uint32_t mt = P.tiles_m * P.nprod;
     const std::uint32_t tiles64 = (P.n % 64 == 0) ? mt * (P.n / 64) : 0;
     const std::uint32_t tiles32 = mt * (P.n / 32);
     const bool s2 = P.k % (2 * KC) == 0, s4 = P.k % (4 * KC) == 0;
-    if (tiles64 >= 96) return dispatch(P, 64, 1, s);
-    if (tiles64 >= 48 && s2) return dispatch(P, 64, 2, s);
-    if (tiles64 >= 24 && s4) return dispatch(P, 64, 4, s);
-    if (tiles32 >= 96) return dispatch(P, 32, 1, s);
-    if (tiles32 >= 48 && s2) return dispatch(P, 32, 2, s);
-    if (s4) return dispatch(P, 32, 4, s);
-    if (s2) return dispatch(P, 32, 2, s);
-    return dispatch(P, 32, 1, s);
+    *bn = 32;
+    *split = 1;
+    if (tiles64 >= 96) { *bn = 64; *split = 1; }
+    else if (tiles64 >= 48 && s2) { *bn = 64; *split = 2; }
+    else if (tiles64 >= 24 && s4) { *bn = 64; *split = 4; }
+    else if (tiles32 >= 96) { *split = 1; }
+    else if (tiles32 >= 48 && s2) { *split = 2; }
+    else if (s4) { *split = 4; }
+    else if (s2) { *split = 2; }
+}
+
+cudaError_t launch_gemm_i8(const GemmParams& P, cudaStream_t s) {
+    if (!gemm_i8_supported(P)) return cudaErrorInvalidValue;
+    int bn, split;
+    gemm_choose(P, &bn, &split);
+    return dispatch(P, bn, split, s);
 }
 
 cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s) {
     if (!leaf_i8_supported(P)) return cudaErrorInvalidValue;
     return launch_gemm_i8(from_mul(P), s);
 }
+
+GemmParams gemm_from_mul(const MulParams& P) { return from_mul(P); }
 
 // measurement hook: force a (BN, SPLIT) configuration
 cudaError_t launch_leaf_i8_cfg(const MulParams& P, int bn, int split, cudaStream_t s) {

@@ -30,6 +30,7 @@ namespace wm {
 cudaError_t launch_leaf_i8(const MulParams& P, cudaStream_t s);      // wm_i8.cu
 bool leaf_i8_supported(const MulParams& P);
 cudaError_t leaf_i8_init();
+GemmParams gemm_from_mul(const MulParams& P);
 cudaError_t launch_leaf_i8_cfg(const MulParams& P, int bn, int split, cudaStream_t s);
 bool frame_kernel_available();
 }  // namespace wm
@@ -62,8 +63,11 @@ struct Step {
     int gid = -1;  // GROUP: fused schedule run
     fused::GroupParams grp;
     FramePrepParams fprep;  // fused leaf frame, three launches
-    GemmParams fgemm;
+    GemmParams fgemm;       // FGEMM, and MUL with leaf == 1 (int8 engine)
     FrameCombParams fcomb;
+    int engine = 0;         // int8 GEMM: 0 cp.async, 1 TMA
+    int bn = 32, split = 1;
+    std::shared_ptr<TmaMaps> tmaps;
 };
 
 struct CachedPlan {
@@ -92,6 +96,7 @@ struct wm_ctx {
     bool batch_adds = true;
     int leaf_kernel = 2;  // 0 dmma, 1 i8, 2 auto (i8 where the tiles fit, else dmma)
     int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames, 4/5/6 frame prep/gemm/comb
+    int gemm_engine = 0;  // int8 GEMM operand path: 0 cp.async ring, 1 TMA tensor maps
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
@@ -251,8 +256,22 @@ bool try_group(const Plan& plan, std::size_t i, int g, double* const base[4], St
     return true;
 }
 
+// Choose tiling and (TMA engine) encode the operand tensor maps for an int8 GEMM step.
+void finish_gemm_step(Step& st, int engine) {
+    gemm_choose(st.fgemm, &st.bn, &st.split);
+    st.engine = 0;
+    if (engine == 1) {
+        auto maps = std::make_shared<TmaMaps>();
+        if (gemm_tma_encode(st.fgemm, st.bn, *maps)) {
+            st.tmaps = maps;
+            st.engine = 1;
+        }
+    }
+}
+
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
-void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps) {
+void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
+                 int engine) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
@@ -313,6 +332,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     G.beta = 0;
     G.pd = pd;
     G.pinv = pinv;
+    finish_gemm_step(g, engine);
     steps.push_back(g);
 
     Step cb{};
@@ -383,7 +403,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         flush();
         if (op.kind == OP_FRAME) {
-            lower_frame(op, f, base, steps);
+            lower_frame(op, f, base, steps, ctx.gemm_engine);
             continue;
         }
         Step s{};
@@ -392,6 +412,10 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             s.kind = Step::MUL;
             const bool i8ok = !f.real && leaf_i8_supported(s.mul);
             s.leaf = (ctx.leaf_kernel == 1 || ctx.leaf_kernel == 2) && i8ok ? 1 : 0;
+            if (s.leaf == 1) {
+                s.fgemm = gemm_from_mul(s.mul);
+                finish_gemm_step(s, ctx.gemm_engine);
+            }
         }
         steps.push_back(s);
     }
@@ -411,13 +435,20 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
         switch (s.kind) {
             case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
             case Step::MUL:
-                if (s.leaf == 1) WM_CUDA(launch_leaf_i8(s.mul, st));
-                else WM_CUDA(launch_leaf_dmma(s.mul, real, st));
+                if (s.leaf == 1) {
+                    if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
+                    else WM_CUDA(launch_gemm_i8(s.fgemm, st));
+                } else {
+                    WM_CUDA(launch_leaf_dmma(s.mul, real, st));
+                }
                 break;
             case Step::FRAME: break;
             case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
             case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
-            case Step::FGEMM: WM_CUDA(launch_gemm_i8(s.fgemm, st)); break;
+            case Step::FGEMM:
+                if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
+                else WM_CUDA(launch_gemm_i8(s.fgemm, st));
+                break;
             case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
         }
     }
@@ -492,7 +523,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -630,6 +661,8 @@ int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out)
         c->f.p = field == WM_FIELD_REAL64 ? 65521u : p;
         WM_CUDA(cudaSetDevice(device));
         WM_CUDA(leaf_i8_init());
+        const bool tma_ok = gemm_tma_init() == cudaSuccess;
+        c->gemm_engine = tma_ok ? 1 : 0;
         if (stream) {
             c->stream = static_cast<cudaStream_t>(stream);
         } else {
@@ -661,6 +694,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "leaf_kernel") ctx->leaf_kernel = static_cast<int>(value);
         else if (k == "subset") ctx->subset = static_cast<int>(value);
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
+        else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
         ctx->cache.clear();
     });
@@ -675,6 +709,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "leaf_kernel") *value = ctx->leaf_kernel;
         else if (k == "subset") *value = ctx->subset;
         else if (k == "fuse_adds") *value = ctx->fuse_adds;
+        else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else fail(E_INVALID, "unknown option " + k);
     });
 }
@@ -886,9 +921,26 @@ int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, in
         WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         for (int i = 0; i < reps; ++i) {
             cudaError_t e;
-            if (kernel == 1) e = launch_leaf_i8(P, ctx->stream);
-            else if (kernel > 1) e = launch_leaf_i8_cfg(P, kernel / 100, kernel % 100, ctx->stream);
-            else e = launch_leaf_dmma(P, ctx->f.real, ctx->stream);
+            if (kernel >= 10000) {  // TMA engine, forced (bn, split)
+                GemmParams G = gemm_from_mul(P);
+                static TmaMaps M;
+                const int bn = (kernel - 10000) / 100, sp = kernel % 100;
+                e = gemm_tma_encode(G, bn, M) ? launch_gemm_tma(G, M, bn, sp, ctx->stream)
+                                              : cudaErrorInvalidValue;
+            } else if (kernel == 2) {  // TMA engine, automatic tiling
+                GemmParams G = gemm_from_mul(P);
+                static TmaMaps M;
+                int bn, sp;
+                gemm_choose(G, &bn, &sp);
+                e = gemm_tma_encode(G, bn, M) ? launch_gemm_tma(G, M, bn, sp, ctx->stream)
+                                              : cudaErrorInvalidValue;
+            } else if (kernel == 1) {
+                e = launch_leaf_i8(P, ctx->stream);
+            } else if (kernel > 2) {
+                e = launch_leaf_i8_cfg(P, kernel / 100, kernel % 100, ctx->stream);
+            } else {
+                e = launch_leaf_dmma(P, ctx->f.real, ctx->stream);
+            }
             if (e != cudaSuccess) {
                 cudaGraph_t g2;
                 cudaStreamEndCapture(ctx->stream, &g2);

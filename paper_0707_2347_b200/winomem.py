@@ -254,8 +254,9 @@ class MatView:
         return MatView(self.mat, self.r0 + r0, self.c0 + c0, r, c)
 
     def dmat(self) -> wm_dmat:
-        base = self.mat.t.data_ptr() + 8 * (self.r0 * self.mat.cols() + self.c0)
-        return wm_dmat(base, self.rows, self.cols, self.mat.cols())
+        ld = self.mat.ld()
+        base = self.mat.t.data_ptr() + 8 * (self.r0 * ld + self.c0)
+        return wm_dmat(base, self.rows, self.cols, ld)
 
     def words(self):
         return self.rows * self.cols
@@ -282,6 +283,24 @@ class Matrix:
         self.real = real
         self.device = device
         self.t = torch.zeros((rows, cols), dtype=torch.float64, device=f"cuda:{device}")
+
+    @classmethod
+    def wrap(cls, t, mod: Optional[Modulus] = None, real=False):
+        """A Matrix over an existing float64 CUDA tensor (row-major, unit column
+        stride; any row stride) -- no copy."""
+        if t.dtype != t.new_zeros(0, dtype=t.dtype).dtype or str(t.dtype) != "torch.float64":
+            raise invalid_argument("wrap expects a float64 tensor")
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise invalid_argument("wrap expects a 2-D tensor with unit column stride")
+        m = cls.__new__(cls)
+        m.mod_ = mod or Modulus(kDefaultModulus)
+        m.real = real
+        m.device = t.device.index or 0
+        m.t = t
+        return m
+
+    def ld(self):
+        return self.t.stride(0)
 
     def ctx(self):
         return Context.get(self.device, self.mod_.p(), self.real)

@@ -20,7 +20,7 @@ for n in (128, 256, 512, 1024):
     A.fill_random(1)
     B.fill_random(2)
     torch.cuda.synchronize()
-    for cfg in (1, 3201, 3202, 3204, 6401, 6402, 6404):
+    for cfg in (1, 2, 3201, 3202, 3204, 6401, 6402, 6404, 13201, 13202, 13204, 16401, 16402, 16404):
         v = C.c_double()
         rc = L.wm_diag_time_leaf(ctx.h, A.view().dmat(), B.view().dmat(), Cm.view().dmat(), 50,
                                  cfg, C.byref(v))

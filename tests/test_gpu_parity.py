@@ -42,12 +42,13 @@ def golden():
 
 
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
-                        dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0)],
-                ids=["default", "nograph", "unfused-i8", "unfused-dmma"])
+                        dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
+                        dict(gemm_engine=0)],
+                ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
-                                              "leaf_kernel", "fuse_adds")}
+                                              "leaf_kernel", "fuse_adds", "gemm_engine")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
@@ -195,11 +196,15 @@ def test_real64_winograd_frobenius(W, O):
 @pytest.mark.parametrize("shape", [(128, 32, 64), (128, 128, 128), (256, 256, 256),
                                    (384, 96, 192), (512, 1024, 128), (1024, 1024, 1024),
                                    (128, 16384, 64)])
-def test_leaf_i8_vs_oracle(W, O, shape):
-    """tcgen05 int8-limb leaf kernel on tile-aligned shapes (incl. the long-K limb bound)."""
+@pytest.mark.parametrize("engine", [0, 1], ids=["cpasync", "tma"])
+def test_leaf_i8_vs_oracle(W, O, shape, engine):
+    """tcgen05 int8-limb leaf kernel on tile-aligned shapes (incl. the long-K limb bound),
+    both operand engines (cp.async ring, TMA tensor maps)."""
     ctx = W.Context.get()
     saved = ctx.get_option("leaf_kernel")
+    saved_e = ctx.get_option("gemm_engine")
     ctx.set_option("leaf_kernel", 1)
+    ctx.set_option("gemm_engine", engine)
     try:
         m, k, n = shape
         for (al, be) in [(1, 0), (1, 1), (3, 65520), (65520, 7)]:
@@ -212,3 +217,4 @@ def test_leaf_i8_vs_oracle(W, O, shape):
             assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (shape, al, be)
     finally:
         ctx.set_option("leaf_kernel", saved)
+        ctx.set_option("gemm_engine", saved_e)
