@@ -217,6 +217,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_partitioned(args, cfg, rank, world, local)
+        dist.destroy_process_group()
+        return
     real = cfg["field"] == "real"
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
     A = W.Matrix(m, k, device=local, real=real)
@@ -371,6 +374,79 @@ def main():
         print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_partitioned(args, cfg, rank, world, local):
+    """N > 1: the 7 top-level Winograd products of ONE multiplication are spread
+    over the ranks (paper_0707_2347_b200/dist.py; NCCL point-to-point carries
+    operand blocks out and products back); strong scaling, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_0707_2347_b200 as W
+    from paper_0707_2347_b200.dist import (CudaBackend, local_variant, makespan_bound,
+                                           partitioned_multiply)
+
+    real = cfg["field"] == "real"
+    m, k, n = cfg["m"], cfg["k"], cfg["n"]
+    lv = local_variant(cfg["variant"], m // 2, k // 2, n // 2)
+    be = CudaBackend(65521, lv, cfg["cutoff"], local, real=real)
+    dev = f"cuda:{local}"
+    A = B = C = None
+    if rank == 0:
+        Am, Bm, Cm = (W.Matrix(m, k, device=local, real=real), W.Matrix(k, n, device=local, real=real),
+                      W.Matrix(m, n, device=local, real=real))
+        Am.fill_random(cfg["seed"])
+        Bm.fill_random(cfg["seed"] + 1)
+        if cfg["beta"]:
+            Cm.fill_random(cfg["seed"] + 2)
+        A, B, C = Am.t, Bm.t, Cm.t
+    ctxs = W.Context.get(local, 65521, real)
+
+    def step():
+        partitioned_multiply(A, B, C, cfg["alpha"], cfg["beta"], be)
+
+    parity = None
+    step()
+    torch.cuda.synchronize()
+    if rank == 0 and not real:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_hashes.json")))
+        h = "%016x" % Cm.hash()
+        want = gold.get(args.config, {}).get("appendix_a")
+        parity = {"c_hash": h, "golden": want, "ok": h == want}
+        if cfg["beta"]:
+            Cm.fill_random(cfg["seed"] + 2)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_step = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": 2.0 * m * n * k / t_step / 1e9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: SplitMix64 seeds A=%d B=%d C=%d" % (cfg["seed"], cfg["seed"] + 1,
+                                                                   cfg["seed"] + 2),
+            "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
+                       "m": m, "k": k, "n": n, "cutoff": cfg["cutoff"],
+                       "parallelism": f"7-way top-level product partition over {world} GPUs "
+                                      f"(NCCL p2p), local schedule {lv}",
+                       "makespan_bound": makespan_bound(world)},
+            "parity": parity, "clocks": clk.summary(),
+        }))
 
 
 def e2e(W, cfg, args, np, torch):

@@ -100,13 +100,23 @@ __global__ void __launch_bounds__(256) k_frame_prep(const FramePrepParams P) {
         t[2][e] = subm(b22[e], b12[e], p);
         t[3][e] = subm(t2, b21[e], p);
     }
+    // plane value block (r, j..j+3) -> 8 bytes at plane + r*pld + j
+    auto put = [&](int pl, const double (&v)[4]) {
+        if (P.plane[pl])
+            *reinterpret_cast<uint2*>(P.plane[pl] + r * P.pld[pl] + j) =
+                pack(v[0], v[1], v[2], v[3]);
+    };
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        *reinterpret_cast<uint2*>(P.s_host + r * 4 * P.s_ld + 4 * (q + k * c4)) =
-            pack(s[k][0], s[k][1], s[k][2], s[k][3]);
-        *reinterpret_cast<uint2*>(P.t_host + r * 4 * P.t_ld + 4 * (q + k * c4)) =
-            pack(t[k][0], t[k][1], t[k][2], t[k][3]);
+        put(PL_S1 + k, s[k]);
+        put(PL_T1 + k, t[k]);
     }
+    put(PL_A11, a11);
+    put(PL_A12, a12);
+    put(PL_A22, a22);
+    put(PL_B11, b11);
+    put(PL_B21, b21);
+    put(PL_B22, b22);
     if (P.beta != 0) {
         std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]);
 #pragma unroll

@@ -13,14 +13,16 @@ struct FrameQuads {
     std::uint64_t ld;      // shared leading dimension (elements)
 };
 
+// residue planes written by the prep launch, in this order
+enum FramePlane { PL_S1, PL_S2, PL_S3, PL_S4, PL_T1, PL_T2, PL_T3, PL_T4,
+                  PL_A11, PL_A12, PL_A22, PL_B11, PL_B21, PL_B22, PL_COUNT };
+
 struct FramePrepParams {
     FrameQuads A, B, C;
-    std::uint16_t* s_host;  // S1..S4 planes (4 per host row), ld = 4*s_ld
-    std::uint64_t s_ld;     // host leading dimension (float64 elements)
-    std::uint16_t* t_host;  // T1..T4 planes
-    std::uint64_t t_ld;
-    std::uint32_t c;        // quadrant size
-    std::uint32_t beta;     // accumulate: pack beta*C_in into C11 slots
+    std::uint16_t* plane[PL_COUNT];  // nullptr: not materialised (raw blocks only)
+    std::uint64_t pld[PL_COUNT];     // plane leading dimension (uint16 elements)
+    std::uint32_t c;                 // quadrant size
+    std::uint32_t beta;              // accumulate: pack beta*C_in into C11 slots
     double pd, pinv;
 };
 

@@ -506,7 +506,7 @@ void multiply_into(const std::string& variant, const View& A, const View& B, con
         const std::uint64_t c = A.rows / 2;
         std::vector<View> hosts;
         for (const View& t : temps)
-            if (t.rows >= c && t.cols >= c && hosts.size() < 2) hosts.push_back(t.window(0, 0, c, c));
+            if (t.rows >= c && t.cols >= c && hosts.size() < 3) hosts.push_back(t.window(0, 0, c, c));
         const bool ovA = s.contract == Contract::OverwriteA || s.contract == Contract::OverwriteBoth;
         const bool ovB = s.contract == Contract::OverwriteB || s.contract == Contract::OverwriteBoth;
         if (hosts.size() < 2 && ovA) hosts.push_back(quad_split(A)[2]);
@@ -526,6 +526,7 @@ void multiply_into(const std::string& variant, const View& A, const View& B, con
             op.row = ctx.row;
             op.h0 = hosts[0];
             op.h1 = hosts[1];
+            if (hosts.size() > 2) op.h2 = hosts[2];
             ctx.out->push_back(op);
         }
         return;

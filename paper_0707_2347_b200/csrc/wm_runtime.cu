@@ -303,10 +303,42 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     p.fprep.A.ld = op.a.ld;
     p.fprep.B.ld = op.b.ld;
     p.fprep.C.ld = op.d.ld;
-    p.fprep.s_host = reinterpret_cast<std::uint16_t*>(ptr(sh));
-    p.fprep.s_ld = sh.ld;
-    p.fprep.t_host = reinterpret_cast<std::uint16_t*>(ptr(th));
-    p.fprep.t_ld = th.ld;
+    // raw blocks materialised as uint16 planes where a free host slot exists:
+    // plain frames own C21, C22 until the combine; accumulating frames own C22
+    // (its beta*C_in is packed away first), a third temporary and the spare
+    // slot of the second product host
+    std::vector<std::pair<View, int>> raw_slots;
+    if (!acc) {
+        for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[2], q});
+        for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[3], q});
+    } else {
+        for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[3], q});
+        if (op.h2.rows) for (int q = 0; q < 4; ++q) raw_slots.push_back({op.h2, q});
+        raw_slots.push_back({op.h1, 3});
+    }
+    const View raw_view[6] = {aq[0], aq[1], aq[3], bq[0], bq[2], bq[3]};
+    GemmSrc raw[6];
+    for (int i = 0; i < 6; ++i) {
+        if (i < static_cast<int>(raw_slots.size())) {
+            raw[i] = plane(raw_slots[i].first, raw_slots[i].second);
+            p.fprep.plane[PL_A11 + i] = const_cast<std::uint16_t*>(
+                static_cast<const std::uint16_t*>(raw[i].p));
+            p.fprep.pld[PL_A11 + i] = raw[i].ld;
+        } else {
+            raw[i] = f64(raw_view[i]);
+            p.fprep.plane[PL_A11 + i] = nullptr;
+        }
+    }
+    GemmSrc st[8];
+    for (int q = 0; q < 4; ++q) {
+        st[q] = plane(sh, q);
+        st[4 + q] = plane(th, q);
+    }
+    for (int i = 0; i < 8; ++i) {
+        p.fprep.plane[PL_S1 + i] = const_cast<std::uint16_t*>(
+            static_cast<const std::uint16_t*>(st[i].p));
+        p.fprep.pld[PL_S1 + i] = st[i].ld;
+    }
     p.fprep.c = static_cast<std::uint32_t>(c);
     p.fprep.beta = op.sb.r;
     p.fprep.pd = pd;
@@ -317,13 +349,14 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     g.kind = Step::FGEMM;
     GemmParams& G = g.fgemm;
     // P1 = A11 B11, P2 = A12 B21, P3 = S4 B22, P4 = A22 T4, P5 = S1 T1, P6 = S2 T2, P7 = S3 T3
-    G.a[0] = f64(aq[0]);   G.b[0] = f64(bq[0]);
-    G.a[1] = f64(aq[1]);   G.b[1] = f64(bq[2]);
-    G.a[2] = plane(sh, 3); G.b[2] = f64(bq[3]);
-    G.a[3] = f64(aq[3]);   G.b[3] = plane(th, 3);
-    G.a[4] = plane(sh, 0); G.b[4] = plane(th, 0);
-    G.a[5] = plane(sh, 1); G.b[5] = plane(th, 1);
-    G.a[6] = plane(sh, 2); G.b[6] = plane(th, 2);
+    // raw[] = {A11, A12, A22, B11, B21, B22} (uint16 planes or float64 blocks)
+    G.a[0] = raw[0]; G.b[0] = raw[3];
+    G.a[1] = raw[1]; G.b[1] = raw[4];
+    G.a[2] = st[3];  G.b[2] = raw[5];
+    G.a[3] = raw[2]; G.b[3] = st[7];
+    G.a[4] = st[0];  G.b[4] = st[4];
+    G.a[5] = st[1];  G.b[5] = st[5];
+    G.a[6] = st[2];  G.b[6] = st[6];
     for (int k = 0; k < 7; ++k) G.c[k] = k < 4 ? plane(op.h0, k) : plane(op.h1, k - 4);
     G.m = G.n = G.k = static_cast<std::uint32_t>(c);
     G.nprod = 7;

@@ -127,8 +127,9 @@ struct Op {
     int frame = -1;
     const char* sched = nullptr;
     int row = 0;
-    // OP_FRAME: the two c x c blocks that host the seven product planes
-    View h0, h1;
+    // OP_FRAME: c x c blocks free for residue planes: h0, h1 host the seven
+    // product planes, h2 (optional, rows == 0 if absent) a third temporary
+    View h0, h1, h2;
 };
 
 // CostMeter (meter.hpp:24-50)

@@ -75,18 +75,20 @@ class CudaBackend:
     """libwinomem_b200 on this rank's GPU: block combinations with the block
     addition kernels, products with the single-GPU memory-lean plan."""
 
-    def __init__(self, p: int, variant: str, cutoff: int, device: int):
+    def __init__(self, p: int, variant: str, cutoff: int, device: int, real: bool = False):
         from . import winomem as W
         self.W = W
-        self.p, self.variant, self.cutoff, self.device = p, variant, cutoff, device
+        self.p, self.variant, self.cutoff, self.device, self.real = p, variant, cutoff, device, real
+        # REAL64 primitives read the uint32 scalar as a signed int32
+        self.m = (1 << 32) if real else p
 
     def _mat(self, t: torch.Tensor):
-        return self.W.Matrix.wrap(t, self.W.Modulus(self.p))  # strided views are fine
+        return self.W.Matrix.wrap(t, self.W.Modulus(self.p), real=self.real)
 
     def lincomb(self, coefs, blocks):
         W = self.W
         out = torch.empty_like(blocks[0])
-        terms = [(c % self.p, b) for c, b in zip(coefs, blocks) if c]
+        terms = [(c % self.m, b) for c, b in zip(coefs, blocks) if c]
         O = self._mat(out)
         first = True
         for c, b in terms:
@@ -104,14 +106,17 @@ class CudaBackend:
                            alpha=1, beta=0, cutoff=self.cutoff)
         return out
 
+    def zero(self, Cq):
+        Cq.zero_()
+
     def fold(self, Cq, coef, P):
         M = self._mat(Cq)
-        self.W.block_addsub(M.view(), M.view(), self._mat(P).view(), 1, coef % self.p)
+        self.W.block_addsub(M.view(), M.view(), self._mat(P).view(), 1, coef % self.m)
 
     def finish(self, Cq, acc, alpha, beta):
         M = self._mat(Cq)
-        self.W.block_addsub(M.view(), self._mat(acc).view(), M.view(), alpha % self.p,
-                            beta % self.p)
+        self.W.block_addsub(M.view(), self._mat(acc).view(), M.view(), alpha % self.m,
+                            beta % self.m)
 
 
 def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, root: int = 0):
@@ -186,6 +191,15 @@ def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, ro
         local[i] = P
         dist.send(P, dst=root, group=group)
     return local
+
+
+def local_variant(variant: str, m: int, k: int, n: int) -> str:
+    """Schedule for the plain products P_i = S_i T_i on each rank."""
+    if variant == "ipmm":
+        return "ipmm"
+    if variant in ("ip", "ovl", "ovl2", "ovr", "iprect", "ipovmm", "aclr"):
+        return "ip" if m == k == n else "iprect"
+    return "std2"
 
 
 def makespan_bound(world: int, products: int = 7) -> float:

@@ -218,3 +218,33 @@ def test_leaf_i8_vs_oracle(W, O, shape, engine):
     finally:
         ctx.set_option("leaf_kernel", saved)
         ctx.set_option("gemm_engine", saved_e)
+
+
+def test_partition_single_rank_gpu(W, O):
+    """The product-partition path (dist.py) with its CUDA backend on one GPU
+    (world size 1, NCCL): block combinations, products and folds all run
+    through libwinomem_b200; bit-exact vs the oracle."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_0707_2347_b200.dist import CudaBackend, partitioned_multiply
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for variant, n, cutoff, al, be in [("std2", 512, 64, 1, 0), ("std2", 1024, 128, 3, 7),
+                                           ("ipmm", 512, 64, 1, 0)]:
+            A, B, C = _problem(W, n, n, n, 31 + n, be != 0)
+            a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+            be_ = CudaBackend(65521, variant, cutoff, 0)
+            partitioned_multiply(A.t, B.t, C.t, al, be, be_)
+            torch.cuda.synchronize()
+            assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (variant, n)
+    finally:
+        dist.destroy_process_group()
