@@ -56,39 +56,51 @@ __device__ __forceinline__ uint2 pack(double a, double b, double c, double d) {
                       static_cast<std::uint32_t>(c) | (static_cast<std::uint32_t>(d) << 16));
 }
 
-// thread (r, q), q < c/4: plane columns j = 4q..4q+3, owned float64 slots
-// (r, q + k c/4) for k = 0..3 of every host / C block.
-__global__ void __launch_bounds__(256) k_frame_prep(const FramePrepParams P) {
+// thread (r, q, h), q < c/4, h in {0,1}: plane columns j = 4q + 2h, +1; the
+// float64 slots (r, q + k c/4), k = 0..3, of every host / C block are owned by
+// the thread pair (q, 0), (q, 1) of one CTA: both read all they need (A, B and
+// beta*C_in) before a barrier, then write their halves of the slots.
+__global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const std::uint32_t c4 = P.c / 4;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<std::uint64_t>(P.c) * c4) return;
-    const std::uint64_t r = idx / c4, q = idx - r * c4, j = 4 * q;
+    const bool live = idx < static_cast<std::uint64_t>(P.c) * c4 * 2;
+    const std::uint64_t pair = idx >> 1, h = idx & 1;
+    const std::uint64_t r = live ? pair / c4 : 0, q = live ? pair - r * c4 : 0;
+    const std::uint64_t j = 4 * q + 2 * h;
     const double p = P.pd, pinv = P.pinv;
 
-    double a11[4], a12[4], a21[4], a22[4], b11[4], b12[4], b21[4], b22[4];
-    ld4(P.A.q[0] + r * P.A.ld + j, a11);
-    ld4(P.A.q[1] + r * P.A.ld + j, a12);
-    ld4(P.A.q[2] + r * P.A.ld + j, a21);
-    ld4(P.A.q[3] + r * P.A.ld + j, a22);
-    ld4(P.B.q[0] + r * P.B.ld + j, b11);
-    ld4(P.B.q[1] + r * P.B.ld + j, b12);
-    ld4(P.B.q[2] + r * P.B.ld + j, b21);
-    ld4(P.B.q[3] + r * P.B.ld + j, b22);
-    // beta * C_in of the four owned slots, read before any host slot is written
-    double cin[4][4];
-    if (P.beta != 0) {
-        const double be = static_cast<double>(P.beta);
+    double a11[2], a12[2], a21[2], a22[2], b11[2], b12[2], b21[2], b22[2];
+    auto ld2 = [&](const double* ptr, double (&v)[2]) {
+        const double2 x = *reinterpret_cast<const double2*>(ptr);
+        v[0] = x.x;
+        v[1] = x.y;
+    };
+    double cin[4][2];  // [k][quadrant 2h, 2h+1]
+    if (live) {
+        ld2(P.A.q[0] + r * P.A.ld + j, a11);
+        ld2(P.A.q[1] + r * P.A.ld + j, a12);
+        ld2(P.A.q[2] + r * P.A.ld + j, a21);
+        ld2(P.A.q[3] + r * P.A.ld + j, a22);
+        ld2(P.B.q[0] + r * P.B.ld + j, b11);
+        ld2(P.B.q[1] + r * P.B.ld + j, b12);
+        ld2(P.B.q[2] + r * P.B.ld + j, b21);
+        ld2(P.B.q[3] + r * P.B.ld + j, b22);
+        if (P.beta != 0) {
+            const double be = static_cast<double>(P.beta);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
-            for (int qd = 0; qd < 4; ++qd)
-                cin[k][qd] = rmod(be * P.C.q[qd][r * P.C.ld + q + k * c4], p, pinv);
+                for (int e = 0; e < 2; ++e)
+                    cin[k][e] = rmod(be * P.C.q[2 * h + e][r * P.C.ld + q + k * c4], p, pinv);
+        }
     }
-    double s[4][4], t[4][4];
+    __syncthreads();  // every owned slot has been read before any is overwritten
+    if (!live) return;
+    double s[4][2], t[4][2];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 2; ++e) {
         const double s1 = addm(a21[e], a22[e], p), s2 = subm(s1, a11[e], p);
         s[0][e] = s1;
         s[1][e] = s2;
@@ -100,11 +112,11 @@ __global__ void __launch_bounds__(256) k_frame_prep(const FramePrepParams P) {
         t[2][e] = subm(b22[e], b12[e], p);
         t[3][e] = subm(t2, b21[e], p);
     }
-    // plane value block (r, j..j+3) -> 8 bytes at plane + r*pld + j
-    auto put = [&](int pl, const double (&v)[4]) {
+    // plane values (r, j..j+1) -> 4 bytes at plane + r*pld + j
+    auto put = [&](int pl, const double (&v)[2]) {
         if (P.plane[pl])
-            *reinterpret_cast<uint2*>(P.plane[pl] + r * P.pld[pl] + j) =
-                pack(v[0], v[1], v[2], v[3]);
+            *reinterpret_cast<std::uint32_t*>(P.plane[pl] + r * P.pld[pl] + j) =
+                static_cast<std::uint32_t>(v[0]) | (static_cast<std::uint32_t>(v[1]) << 16);
     };
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -121,36 +133,33 @@ __global__ void __launch_bounds__(256) k_frame_prep(const FramePrepParams P) {
         std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-            *reinterpret_cast<uint2*>(c11 + 4 * (r * P.C.ld + q + k * c4)) =
-                pack(cin[k][0], cin[k][1], cin[k][2], cin[k][3]);
+            *reinterpret_cast<std::uint32_t*>(c11 + 4 * (r * P.C.ld + q + k * c4) + 2 * h) =
+                static_cast<std::uint32_t>(cin[k][0]) | (static_cast<std::uint32_t>(cin[k][1]) << 16);
     }
 }
 
-// thread (r, 4 consecutive columns j..j+3) of the quadrant
-__global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
+// thread (r, 2 consecutive columns j, j+1) of the quadrant
+__global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    const std::uint32_t c4 = P.c / 4;
+    const std::uint32_t c2 = P.c / 2;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<std::uint64_t>(P.c) * c4) return;
-    const std::uint64_t r = idx / c4, j = 4 * (idx - r * c4);
+    if (idx >= static_cast<std::uint64_t>(P.c) * c2) return;
+    const std::uint64_t r = idx / c2, j = 2 * (idx - r * c2);
     const double p = P.pd, pinv = P.pinv;
-    double pv[7][4];
+    double pv[7][2];
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
-        const uint2 w = *reinterpret_cast<const uint2*>(P.P[k] + r * P.pld[k] + j);
-        pv[k][0] = static_cast<double>(w.x & 0xFFFFu);
-        pv[k][1] = static_cast<double>(w.x >> 16);
-        pv[k][2] = static_cast<double>(w.y & 0xFFFFu);
-        pv[k][3] = static_cast<double>(w.y >> 16);
+        const std::uint32_t w = *reinterpret_cast<const std::uint32_t*>(P.P[k] + r * P.pld[k] + j);
+        pv[k][0] = static_cast<double>(w & 0xFFFFu);
+        pv[k][1] = static_cast<double>(w >> 16);
     }
-    double cin[4][4];  // [col e][quadrant]
+    double cin[2][4];  // [col e][quadrant]
     if (P.beta != 0) {
         const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const uint2 w =
-                *reinterpret_cast<const uint2*>(c11 + 4 * (r * P.C.ld + j + e));
+        for (int e = 0; e < 2; ++e) {
+            const uint2 w = *reinterpret_cast<const uint2*>(c11 + 4 * (r * P.C.ld + j + e));
             cin[e][0] = static_cast<double>(w.x & 0xFFFFu);
             cin[e][1] = static_cast<double>(w.x >> 16);
             cin[e][2] = static_cast<double>(w.y & 0xFFFFu);
@@ -158,9 +167,9 @@ __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
         }
     }
     const double al = static_cast<double>(P.alpha);
-    double out[4][4];  // [quadrant][col]
+    double out[4][2];  // [quadrant][col]
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < 2; ++e) {
         const double p1 = pv[0][e], p2 = pv[1][e], p3 = pv[2][e], p4 = pv[3][e],
                      p5 = pv[4][e], p6 = pv[5][e], p7 = pv[6][e];
         const double u2 = p1 + p6;
@@ -174,18 +183,15 @@ __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
         }
     }
 #pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-        double* dst = P.C.q[qd] + r * P.C.ld + j;
-        *reinterpret_cast<double2*>(dst) = make_double2(out[qd][0], out[qd][1]);
-        *reinterpret_cast<double2*>(dst + 2) = make_double2(out[qd][2], out[qd][3]);
-    }
+    for (int qd = 0; qd < 4; ++qd)
+        *reinterpret_cast<double2*>(P.C.q[qd] + r * P.C.ld + j) = make_double2(out[qd][0], out[qd][1]);
 }
 
 template <class K, class Prm>
 cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>((threads + 255) / 256));
-    cfg.blockDim = dim3(256);
+    cfg.gridDim = dim3(static_cast<unsigned>((threads + 127) / 128));
+    cfg.blockDim = dim3(128);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -198,11 +204,11 @@ cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t
 }  // namespace
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
-    return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 4), s);
+    return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
 }
 
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s) {
-    return launch_pdl(k_frame_comb, P, static_cast<std::uint64_t>(P.c) * (P.c / 4), s);
+    return launch_pdl(k_frame_comb, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
 }
 
 bool frame_kernel_available() { return true; }
