@@ -229,6 +229,10 @@ def main():
     ctx.set_option("leaf_kernel", args.leaf)
     ctx.set_option("fuse_frames", args.fuse)
     ctx.set_option("graphs", 1)
+    if os.environ.get("WM_FRAME_CFG"):
+        ctx.set_option("frame_cfg", int(os.environ["WM_FRAME_CFG"]))
+    if os.environ.get("WM_GEMM_ENGINE"):
+        ctx.set_option("gemm_engine", int(os.environ["WM_GEMM_ENGINE"]))
 
     def reset_inputs():
         A.fill_random(cfg["seed"])
@@ -310,24 +314,38 @@ def main():
     t_frame = subset_time(3) if rep.fused_frames else 0.0
     frame_parts = ({"prep": subset_time(4), "gemm": subset_time(5), "comb": subset_time(6)}
                    if rep.fused_frames else {})
+
     hbm, hbm_src = peaks()
-    add_issued = rep.add_bytes_issued
     comps = {"additions": t_add, "leaf_products": t_leaf, "fused_frames": t_frame}
     dominant = max(comps, key=comps.get)
-    if dominant == "additions":
-        achieved = add_issued / t_add / 1e9 if t_add else 0.0
-        roof = {"bound": "hbm", "kernel": "k_addsub (batched block additions)",
-                "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "peak_source": hbm_src,
-                "algorithmic_bytes_per_step": add_issued, "kernel_seconds_per_step": t_add}
-    else:
-        # leaf / frame products: effective (2mnk of the leaves) rate; the
-        # tensor-pipe peak is the measured int8 / DMMA figure when available
-        t = comps[dominant]
-        achieved = rep.leaf_flops / t / 1e12 if t else 0.0
-        roof = {"bound": "tensor", "kernel": dominant, "achieved": achieved, "peak": None,
-                "unit": "TFLOP/s", "frac": None, "traffic": None,
-                "algorithmic_flops_per_step": rep.leaf_flops, "kernel_seconds_per_step": t}
+    # every class is bound by HBM / L2 bytes at these sizes (the int8 tensor work
+    # is 4 x 2mnk limb ops against >= 4 POPS): report bytes over measured time
+    rooflines = {
+        "additions": {"bound": "hbm", "kernel": "k_group / k_addsub (block additions)",
+                      "algorithmic_bytes_per_step": rep.add_bytes_issued, "seconds_per_step": t_add},
+        "fused_frames": {"bound": "hbm",
+                         "kernel": "fused leaf frames (k_frame_prep + k_gemm_tma + k_frame_comb)",
+                         "algorithmic_bytes_per_step": rep.frame_bytes,
+                         "seconds_per_step": t_frame},
+        "frame_gemm": {"bound": "hbm", "kernel": "k_gemm_tma (7 leaf products per launch)",
+                       "algorithmic_bytes_per_step": rep.frame_gemm_bytes,
+                       "seconds_per_step": frame_parts.get("gemm", 0.0),
+                       "int8_ops_per_step": 4 * rep.leaf_flops},
+        "leaf_products": {"bound": "hbm", "kernel": "k_gemm (unfused leaves)",
+                          "algorithmic_bytes_per_step": None, "seconds_per_step": t_leaf},
+    }
+    for r_ in rooflines.values():
+        b, t = r_["algorithmic_bytes_per_step"], r_["seconds_per_step"]
+        r_["achieved"] = b / t / 1e9 if b and t else None
+        r_["peak"] = hbm
+        r_["unit"] = "GB/s"
+        r_["frac"] = r_["achieved"] / hbm if r_["achieved"] else None
+    dom = rooflines[dominant]
+    roof = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
+            "peak": hbm, "unit": "GB/s", "frac": dom["frac"], "traffic": None,
+            "peak_source": hbm_src,
+            "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
+            "kernel_seconds_per_step": dom["seconds_per_step"]}
 
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
@@ -353,6 +371,7 @@ def main():
         "parity": parity,
         "breakdown_s": comps,
         "frame_breakdown_s": frame_parts,
+        "rooflines": rooflines,
         "roofline": roof,
         "gpu_launches": rep.n_launches * args.steps,
         "launches_per_step": rep.n_launches,

@@ -78,6 +78,11 @@ typedef struct {
     uint64_t leaf_flops;
     /* bytes the issued addition kernels move (fused frames keep theirs on chip) */
     uint64_t add_bytes_issued;
+    /* fused frames: algorithmic bytes of the seven-product GEMM launches (each
+     * operand plane / block read once, each product plane written once) and of
+     * the whole frames (A, B, beta*C read once, C written once) */
+    uint64_t frame_gemm_bytes;
+    uint64_t frame_bytes;
 } wm_report;
 
 /* ---- library / context --------------------------------------------------- */

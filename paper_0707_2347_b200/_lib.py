@@ -35,7 +35,8 @@ class wm_report(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "mults", "adds", "peak_extra_words", "total_alloc_words", "word_moves",
         "classical_calls", "schedule_frames", "peak_extra_bytes", "n_ops", "n_launches",
-        "fused_frames", "add_bytes", "leaf_flops", "add_bytes_issued")]
+        "fused_frames", "add_bytes", "leaf_flops", "add_bytes_issued", "frame_gemm_bytes",
+        "frame_bytes")]
 
 
 _lib = None

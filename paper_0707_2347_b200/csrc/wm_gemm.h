@@ -25,6 +25,7 @@ struct GemmParams {
     std::uint32_t tiles_m;   // m / 128
     std::uint32_t alpha, beta;  // float64 outputs only
     double pd, pinv;
+    unsigned long long* trace;  // diagnostics: per-CTA phase timestamps (nullptr: off)
 };
 
 // TMA operand maps (one pair per product), encoded on the host at lowering time

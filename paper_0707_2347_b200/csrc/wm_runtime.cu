@@ -97,6 +97,7 @@ struct wm_ctx {
     int leaf_kernel = 2;  // 0 dmma, 1 i8, 2 auto (i8 where the tiles fit, else dmma)
     int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames, 4/5/6 frame prep/gemm/comb
     int gemm_engine = 0;  // int8 GEMM operand path: 0 cp.async ring, 1 TMA tensor maps
+    int frame_cfg = 0;    // measurement: force the frame GEMM tiling (100*BN + split)
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
@@ -257,8 +258,12 @@ bool try_group(const Plan& plan, std::size_t i, int g, double* const base[4], St
 }
 
 // Choose tiling and (TMA engine) encode the operand tensor maps for an int8 GEMM step.
-void finish_gemm_step(Step& st, int engine) {
+void finish_gemm_step(Step& st, int engine, int force = 0) {
     gemm_choose(st.fgemm, &st.bn, &st.split);
+    if (force) {
+        st.bn = force / 100;
+        st.split = force % 100;
+    }
     st.engine = 0;
     if (engine == 1) {
         auto maps = std::make_shared<TmaMaps>();
@@ -271,7 +276,7 @@ void finish_gemm_step(Step& st, int engine) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine) {
+                 int engine, int force) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
@@ -365,7 +370,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     G.beta = 0;
     G.pd = pd;
     G.pinv = pinv;
-    finish_gemm_step(g, engine);
+    finish_gemm_step(g, engine, force);
     steps.push_back(g);
 
     Step cb{};
@@ -436,7 +441,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         flush();
         if (op.kind == OP_FRAME) {
-            lower_frame(op, f, base, steps, ctx.gemm_engine);
+            lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg);
             continue;
         }
         Step s{};
@@ -510,6 +515,20 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                     r->add_bytes_issued += (s.add.it[i].mode <= M_GEN ? 3 : 2) *
                                            static_cast<std::uint64_t>(s.add.it[i].rows) *
                                            s.add.it[i].cols * sizeof(double);
+            if (s.kind == Step::FGEMM) {
+                const GemmParams& G = s.fgemm;
+                const std::uint64_t mk = static_cast<std::uint64_t>(G.m) * G.k,
+                                    kn = static_cast<std::uint64_t>(G.k) * G.n,
+                                    mn = static_cast<std::uint64_t>(G.m) * G.n;
+                for (std::uint32_t i = 0; i < G.nprod; ++i)
+                    r->frame_gemm_bytes += mk * (G.a[i].fmt == 1 ? 2 : 8) +
+                                           kn * (G.b[i].fmt == 1 ? 2 : 8) +
+                                           mn * (G.c[i].fmt == 1 ? 2 : 8);
+            }
+            if (s.kind == Step::FPREP) {
+                const std::uint64_t c2 = static_cast<std::uint64_t>(s.fprep.c) * s.fprep.c;
+                r->frame_bytes += (4 + 4 + 4 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double);
+            }
             if (s.kind == Step::GROUP) {
                 const fused::GroupDesc& G = fused::kGroups[s.gid];
                 r->add_bytes_issued += static_cast<std::uint64_t>(G.nload + G.nstore) *
@@ -556,7 +575,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -728,6 +747,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "subset") ctx->subset = static_cast<int>(value);
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
+        else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
         ctx->cache.clear();
     });
@@ -743,6 +763,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "subset") *value = ctx->subset;
         else if (k == "fuse_adds") *value = ctx->fuse_adds;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
+        else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
     });
 }
@@ -888,14 +909,12 @@ int wm_plan_report(const char* variant, int field, uint32_t p, uint64_t m, uint6
         Scalar a = f.real ? real_scalar(alpha) : modp_scalar(f, alpha);
         Scalar b = f.real ? real_scalar(beta) : modp_scalar(f, beta);
         Plan plan = plan_variant(variant ? variant : "", f, m, k, n, k, n, n, a, b, cutoff, opt);
-        fill_report(plan, nullptr, report);
-        if (report) {
-            // launches as lowered with batching (pointer-free count)
-            wm_ctx dummy;
-            dummy.batch_adds = true;
-            double* base[4] = {nullptr, nullptr, nullptr, nullptr};
-            report->n_launches = lower(plan, base, dummy).size();
-        }
+        // lowered as a context would (pointer-free: counts and byte figures only)
+        wm_ctx dummy;
+        dummy.gemm_engine = 0;
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        const std::vector<Step> steps = lower(plan, base, dummy);
+        fill_report(plan, &steps, report);
     });
 }
 
@@ -998,6 +1017,69 @@ int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, in
         cudaEventDestroy(e1);
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
+    });
+}
+
+// Diagnostics: the seven-product frame GEMM on uint16 planes of a c x c frame,
+// forced tiling cfg (100*bn + split; 0 = automatic), timed over `reps` graph-
+// replayed launches; trace_out (optional, 16 x #CTAs u64) gets one traced launch.
+int wm_diag_frame_gemm(wm_ctx* ctx, uint32_t c, int cfg, int reps, double* us,
+                       unsigned long long* trace_out, int* nctas) {
+    return guard([&] {
+        const std::size_t plane = static_cast<std::size_t>(c) * c;
+        std::uint16_t* buf = nullptr;
+        WM_CUDA(cudaMalloc(&buf, 21 * plane * sizeof(std::uint16_t)));
+        WM_CUDA(cudaMemset(buf, 1, 21 * plane * sizeof(std::uint16_t)));
+        GemmParams G{};
+        for (int k = 0; k < 7; ++k) {
+            G.a[k] = {buf + (3 * k) * plane, c, 1};
+            G.b[k] = {buf + (3 * k + 1) * plane, c, 1};
+            G.c[k] = {buf + (3 * k + 2) * plane, c, 1};
+        }
+        G.m = G.n = G.k = c;
+        G.nprod = 7;
+        G.tiles_m = c / 128;
+        G.alpha = 1;
+        G.pd = static_cast<double>(ctx->f.p);
+        G.pinv = 1.0 / G.pd;
+        Step st{};
+        st.fgemm = G;
+        finish_gemm_step(st, 1, cfg);
+        if (st.engine != 1) fail(E_INVALID, "TMA engine unavailable");
+        *nctas = st.split * static_cast<int>(G.n / st.bn) * static_cast<int>(G.tiles_m * 7);
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < reps; ++i) launch_gemm_tma(st.fgemm, *st.tmaps, st.bn, st.split, ctx->stream);
+        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, ctx->stream);
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEventRecord(e1, ctx->stream);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *us = 1000.0 * ms / reps;
+        if (trace_out) {
+            unsigned long long* dtr = nullptr;
+            const std::size_t n = static_cast<std::size_t>(*nctas) * 16;
+            WM_CUDA(cudaMalloc(&dtr, n * sizeof(unsigned long long)));
+            WM_CUDA(cudaMemset(dtr, 0, n * sizeof(unsigned long long)));
+            st.fgemm.trace = dtr;
+            WM_CUDA(launch_gemm_tma(st.fgemm, *st.tmaps, st.bn, st.split, ctx->stream));
+            WM_CUDA(cudaStreamSynchronize(ctx->stream));
+            WM_CUDA(cudaMemcpy(trace_out, dtr, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            cudaFree(dtr);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        cudaFree(buf);
     });
 }
 

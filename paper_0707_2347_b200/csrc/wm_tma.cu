@@ -146,6 +146,19 @@ __device__ __forceinline__ void tmem_rows16(std::uint32_t taddr, double (&v)[16]
     }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// diagnostics: phase timestamps of one thread per CTA
+#define WM_STAMP(slot)                                                                   \
+    do {                                                                                 \
+        if (P.trace)                                                                     \
+            P.trace[(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) * 16 + \
+                    (slot)] = gtimer();                                                  \
+    } while (0)
+
 template <int BN, int SPLIT>
 __global__ void __launch_bounds__(NT, 1)
     k_gemm_tma(const __grid_constant__ GemmParams P, const __grid_constant__ TmaMaps M) {
@@ -166,6 +179,7 @@ __global__ void __launch_bounds__(NT, 1)
     const GemmSrc Cd = P.c[prod];
     const bool out16 = Cd.fmt == 1;
 
+    if (tid == 64) WM_STAMP(0);
     if (warp == 0) tc::tmem_alloc(&S.tmem_base, TCOLS);
     if (tid == 32) {
         for (int s = 0; s < NF; ++s) {
@@ -183,8 +197,10 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
     tc::fence_after();
     const std::uint32_t tbase = S.tmem_base;
+    if (tid == 64) WM_STAMP(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (tid == 64) WM_STAMP(2);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -232,6 +248,7 @@ __global__ void __launch_bounds__(NT, 1)
         for (std::uint32_t kc = 0; kc < nk; ++kc) {
             const int st = kc % NF, ls = kc % NLIMB;
             tc::mbar_wait(&S.full[st], (kc / NF) & 1);
+            if (ct == 0 && kc == 0) WM_STAMP(3);
             if (kc >= static_cast<std::uint32_t>(NLIMB))
                 tc::mbar_wait(&S.lempty[ls], ((kc / NLIMB) - 1) & 1);
             convert_a(S.a[st], S.a_hi[ls], S.a_lo[ls], ct, a16);
@@ -247,10 +264,12 @@ __global__ void __launch_bounds__(NT, 1)
 
     const double p = P.pd, pinv = P.pinv;
     const double al = static_cast<double>(P.alpha), be = static_cast<double>(P.beta);
+    if (tid == 64) WM_STAMP(4);
     if (warp >= 2) {
         tc::mbar_wait(&S.done, 0);
         tc::fence_after();
     }
+    if (tid == 64) WM_STAMP(5);
     const int lg = warp & 3, half = (warp - 2) >> 2;
     const std::uint32_t row = lg * 32 + lane;
     const std::uint32_t lane_off = static_cast<std::uint32_t>(lg * 32) << 16;
@@ -321,7 +340,9 @@ __global__ void __launch_bounds__(NT, 1)
                                                            j0 + c];
             }
         }
+        if (tid == 64) WM_STAMP(6);
         cluster.sync();
+        if (tid == 64) WM_STAMP(7);
         if (warp >= 2) {
             const std::uint32_t* src[SPLIT];
 #pragma unroll
@@ -353,11 +374,14 @@ __global__ void __launch_bounds__(NT, 1)
                 }
             }
         }
+        if (tid == 64) WM_STAMP(8);
         cluster.sync();
     }
+    if (tid == 64) WM_STAMP(9);
     tc::fence_before();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc(tbase, TCOLS);
+    if (tid == 64) WM_STAMP(10);
 }
 
 template <int BN>

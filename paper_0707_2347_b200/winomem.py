@@ -158,6 +158,8 @@ class CostReport:
     add_bytes: int = 0
     leaf_flops: int = 0
     add_bytes_issued: int = 0
+    frame_gemm_bytes: int = 0
+    frame_bytes: int = 0
 
     def ops(self):
         return self.mults + self.adds
@@ -182,7 +184,7 @@ def _report(variant, m, k, n, cutoff, r: wm_report) -> CostReport:
     return CostReport(variant, m, k, n, cutoff, r.mults, r.adds, r.peak_extra_words,
                       r.total_alloc_words, r.word_moves, r.classical_calls, calls,
                       r.peak_extra_bytes, r.n_ops, r.n_launches, r.fused_frames, r.add_bytes,
-                      r.leaf_flops, r.add_bytes_issued)
+                      r.leaf_flops, r.add_bytes_issued, r.frame_gemm_bytes, r.frame_bytes)
 
 
 # ---- device context ------------------------------------------------------
