@@ -1,0 +1,423 @@
+// Direct-limb product kernel of the fused leaf frames.
+//
+// The frame prep kernel (wm_frame.cu) writes every GEMM operand as a pair of
+// byte planes -- the high and low 8-bit limbs of the residues, a = 256 a_h + a_l
+// -- side by side in one row of its host block (hi bytes [0, c), lo bytes
+// [c, 2c)).  That is exactly the form the tensor cores consume, so this kernel
+// has no conversion stage at all:
+//
+//   * one elected thread streams 128-deep K stages with TWO tensor-map TMA loads
+//     per stage: A as a 3-D box {128 K bytes, 128 rows, 2 limbs} in 128-B swizzle
+//     (the canonical K-major SW128 UMMA layout) and B as {BN bytes, 128 K rows,
+//     2 limbs} in BN-byte swizzle (the canonical MN-major layout, so B needs no
+//     transpose);
+//   * one thread issues the 4 K-steps x 4 limb MMAs of a stage
+//     (tcgen05.mma kind::i8 into the hh / cross / ll TMEM accumulators, the
+//     arithmetic contract of wm_i8.cu) and commits them to the stage's "empty"
+//     barrier;
+//   * four warps read the accumulators back, recombine 2^16 hh + 2^8 x + ll
+//     exactly in float64, reduce mod p and store uint16 product planes.
+//
+// Stage size is what matters on this part: a TMA load costs ~0.3 us of latency
+// per ring slot almost independently of its size (scripts/tma_probe.cu), so the
+// ring carries 40-48 KB stages rather than 10 KB ones.
+//
+// A product whose B operand could not be given a plane (the B22 block of an
+// accumulating frame with only two temporaries) is read as float64 residues by
+// the four epilogue warps, which split it into the same swizzled limb layout
+// while the TMA brings A.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "wm_gemm.h"
+#include "wm_tc.h"
+
+namespace wm {
+namespace {
+
+constexpr int BM = 128, KT = 128, NS = 4;
+constexpr int NEPI = 256;           // eight epilogue / B-loader warps
+constexpr int NT = 64 + NEPI;      // + TMA producer warp + MMA warp
+constexpr int A_PART = BM * KT;  // 16 KB per limb
+
+template <int BN>
+struct DCfg {
+    static constexpr int B_PART = KT * BN;
+    static constexpr int STAGE = 2 * A_PART + 2 * B_PART;  // 40 KB (BN 32) / 48 KB (BN 64)
+    static constexpr std::uint32_t TCOLS = BN == 32 ? 128 : 256;
+    // UMMA layout type of the MN-major B tile (swizzle span = BN bytes)
+    static constexpr std::uint64_t B_LAYOUT = BN == 32 ? 6 : 4;  // SWIZZLE_32B / SWIZZLE_64B
+};
+
+template <int BN>
+struct DSmem {
+    std::uint8_t stage[NS][DCfg<BN>::STAGE];  // 1024-B aligned
+    std::uint64_t full[NS], empty[NS];
+    std::uint64_t done;
+    std::uint32_t tmem_base;
+};
+
+__device__ __forceinline__ double reduce_modp(double v, double p, double pinv) {
+    const double q = floor(v * pinv);
+    double r = fma(-q, p, v);
+    r = r < 0.0 ? r + p : r;
+    return r >= p ? r - p : r;
+}
+
+// swizzled shared-memory descriptor: start, LBO, SBO (bytes), layout type
+__device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr, std::uint32_t lbo,
+                                               std::uint32_t sbo, std::uint64_t layout) {
+    std::uint64_t d = 0;
+    d |= static_cast<std::uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<std::uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<std::uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;
+    d |= layout << 61;
+    return d;
+}
+
+// kind::i8, D s32, A/B u8, A K-major, B MN-major
+__host__ __device__ constexpr std::uint32_t idesc_direct(int M, int N) {
+    return (2u << 4) | (1u << 16) | (static_cast<std::uint32_t>(N >> 3) << 17) |
+           (static_cast<std::uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            std::uint64_t* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+        "r"(tc::smem_u32(mbar))
+        : "memory");
+}
+
+// byte offset of B element (k, n) in a BN-byte-swizzled MN-major limb tile
+template <int BN>
+__device__ __forceinline__ std::uint32_t boff(std::uint32_t k, std::uint32_t n) {
+    constexpr std::uint32_t mask = BN == 32 ? 1u : 3u;
+    constexpr std::uint32_t sh = BN == 32 ? 2u : 1u;
+    return k * BN + ((((n >> 4) ^ (k >> sh)) & mask) << 4) + (n & 15u);
+}
+
+// exact uint32 -> float64 without a conversion instruction: 2^52 + u has u in
+// its low mantissa word
+__device__ __forceinline__ double u2d(std::uint32_t u) {
+    return __hiloint2double(0x43300000, static_cast<int>(u)) - 4503599627370496.0;
+}
+
+// 16 accumulator columns of one TMEM lane: D_h = A_h [B_h | B_l] at [0, 2BN),
+// D_l = A_l [B_h | B_l] at [2BN, 4BN); v = 2^16 hh + 2^8 (hl + lh) + ll < 2^50.
+// The residue r = v - q p uses q = rint(v / p) from a magic-constant FMA and one
+// sign fix, and leaves as an integer through the same 2^52 trick: the epilogue
+// runs on the float64 FMA pipe only (no I2F / F2I / FRND, which are 4-16x slower).
+template <int BN>
+__device__ __forceinline__ void tmem_cols16(std::uint32_t taddr, std::uint32_t (&out)[16], double p,
+                                            double pinv) {
+    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52: rint via addition
+    std::uint32_t hh[16], hl[16], lh[16], ll[16];
+    tc::tmem_ld16(taddr, hh);
+    tc::tmem_ld16(taddr + BN, hl);
+    tc::tmem_ld16(taddr + 2 * BN, lh);
+    tc::tmem_ld16(taddr + 3 * BN, ll);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const double x = u2d(hl[e]) + u2d(lh[e]);
+        const double v = fma(u2d(hh[e]), 65536.0, fma(x, 256.0, u2d(ll[e])));
+        const double q = fma(v, pinv, kMagic) - kMagic;
+        double r = fma(-q, p, v);  // exact, |r| <= p/2 + 1
+        r = r < 0.0 ? r + p : r;
+        out[e] = static_cast<std::uint32_t>(__double2loint(r + 4503599627370496.0));
+    }
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// diagnostics: phase timestamps of one thread per CTA (P.trace, 16 slots per CTA)
+#define WM_DSTAMP(slot)                                                                        \
+    do {                                                                                       \
+        if (P.trace) P.trace[(blockIdx.y + gridDim.y * blockIdx.z) * 16 + (slot)] = gtimer(); \
+    } while (0)
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tc::smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(std::uint64_t* mbar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(tc::smem_u32(mbar))
+                 : "memory");
+}
+
+// BSRC: how B limb tiles reach shared memory when B is a plane pair --
+// 0 tensor-map TMA (with A), 1 16-B cp.async by the eight epilogue warps
+template <int BN, int BSRC>
+__global__ void __launch_bounds__(NT, 1)
+    k_gemm_direct(const __grid_constant__ GemmParams P, const __grid_constant__ TmaMaps M) {
+    using C = DCfg<BN>;
+    extern __shared__ std::uint8_t smem_raw[];
+    const std::uint32_t base = tc::smem_u32(smem_raw);
+    DSmem<BN>& S = *reinterpret_cast<DSmem<BN>*>(smem_raw + ((1024 - (base & 1023)) & 1023));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int prod = static_cast<int>(blockIdx.z / P.tiles_m);
+    const std::uint32_t i0 = (blockIdx.z % P.tiles_m) * BM;
+    const std::uint32_t j0 = blockIdx.y * BN;
+    const std::uint32_t nk = P.k / KT;
+    const bool bconv = P.b[prod].fmt == 0;  // float64 B: split by the epilogue warps
+    const bool blsu = !bconv && BSRC == 1;
+    const GemmSrc Cd = P.c[prod];
+
+    if (tid == 32) WM_DSTAMP(0);
+    if (warp == 0) tc::tmem_alloc(&S.tmem_base, C::TCOLS);
+    if (tid == 32) {
+        for (int s = 0; s < NS; ++s) {
+            tc::mbar_init(&S.full[s], bconv ? 1 + NEPI / 32 : (blsu ? 1 + NEPI : 1));
+            tc::mbar_init(&S.empty[s], 1);
+        }
+        tc::mbar_init(&S.done, 1);
+        tc::mbar_fence_init();
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const std::uint32_t tbase = S.tmem_base;
+    if (tid == 32) WM_DSTAMP(1);
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (tid == 32) WM_DSTAMP(2);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const bool btma = !bconv && !blsu;
+            const std::uint32_t bytes = 2 * A_PART + (btma ? 2 * C::B_PART : 0);
+            for (std::uint32_t kc = 0; kc < nk; ++kc) {
+                const int st = kc % NS;
+                if (kc >= static_cast<std::uint32_t>(NS))
+                    tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
+                tc::mbar_arrive_expect_tx(&S.full[st], bytes);
+                const int k0 = static_cast<int>(kc * KT);
+                tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
+                if (btma)
+                    tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0, 0,
+                                &S.full[st]);
+            }
+        }
+    } else if (warp == 1) {
+        // N = 2 BN: the two B limb tiles are adjacent MN atoms (LBO = B_PART)
+        constexpr std::uint32_t idesc = idesc_direct(BM, 2 * BN);
+        for (std::uint32_t kc = 0; kc < nk; ++kc) {
+            const int st = kc % NS;
+            tc::mbar_wait(&S.full[st], (kc / NS) & 1);
+            tc::fence_after();
+            tc::fence_proxy_async();  // cp.async / st.shared limb tiles -> tensor core
+            if (lane == 0 && kc == 0) WM_DSTAMP(3);
+            if (lane == 0 && kc + 1 == nk) WM_DSTAMP(4);
+            if (lane == 0) {
+                const std::uint32_t sa = tc::smem_u32(S.stage[st]);
+                const std::uint32_t sb = sa + 2 * A_PART;
+#pragma unroll
+                for (int s = 0; s < KT / 32; ++s) {
+                    // A: K-major SW128, K step = 32 bytes inside the 128-B swizzle row
+                    const std::uint64_t ah = sdesc(sa + s * 32, 16, 1024, 2);
+                    const std::uint64_t al = sdesc(sa + A_PART + s * 32, 16, 1024, 2);
+                    // B: MN-major, BN-byte swizzle, K step = 32 rows
+                    const std::uint64_t b = sdesc(sb + s * 32 * BN, C::B_PART, 8 * BN, C::B_LAYOUT);
+                    const bool acc = kc > 0 || s > 0;
+                    tc::mma_i8(tbase + 0, ah, b, idesc, acc);
+                    tc::mma_i8(tbase + 2 * BN, al, b, idesc, acc);
+                }
+                tc::commit(&S.empty[st]);
+                if (kc + 1 == nk) tc::commit(&S.done);
+            }
+            __syncwarp();
+        }
+    } else if (blsu) {
+        const int ct = tid - 64;
+        const std::uint8_t* bsrc = static_cast<const std::uint8_t*>(P.b[prod].p);
+        const std::uint64_t pitch = P.b[prod].ld, part = P.b[prod].part;
+        constexpr int CPR = BN / 16;                     // 16-B chunks per limb row
+        constexpr int PER = 2 * KT * CPR / NEPI;         // chunks per thread per stage
+        for (std::uint32_t kc = 0; kc < nk; ++kc) {
+            const int st = kc % NS;
+            if (kc >= static_cast<std::uint32_t>(NS)) tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
+            std::uint8_t* bt = S.stage[st] + 2 * A_PART;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) {
+                const int q = e * NEPI + ct;
+                const int limb = q / (KT * CPR), rem = q % (KT * CPR);
+                const std::uint32_t k = rem / CPR, nc = rem % CPR;
+                cp_async16(bt + limb * C::B_PART + boff<BN>(k, nc * 16),
+                           bsrc + static_cast<std::uint64_t>(kc * KT + k) * pitch + limb * part + j0 + nc * 16);
+            }
+            cp_async_arrive(&S.full[st]);
+        }
+    } else if (bconv) {
+        // float64 B rows [k0, k0 + 128) x [j0, j0 + BN) -> swizzled limb tiles
+        const int ct = tid - 64;
+        const double* bsrc = static_cast<const double*>(P.b[prod].p);
+        const std::uint64_t ldb = P.b[prod].ld;
+        for (std::uint32_t kc = 0; kc < nk; ++kc) {
+            const int st = kc % NS;
+            if (kc >= static_cast<std::uint32_t>(NS)) tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
+            std::uint8_t* bh = S.stage[st] + 2 * A_PART;
+            std::uint8_t* bl = bh + C::B_PART;
+            constexpr int PER = KT * BN / NEPI;
+            constexpr int RSTEP = NEPI / BN;
+            const std::uint32_t n = ct % BN;
+#pragma unroll 8
+            for (int e = 0; e < PER; ++e) {
+                const std::uint32_t k = ct / BN + e * RSTEP;
+                const std::uint32_t v = __double2uint_rz(
+                    bsrc[static_cast<std::uint64_t>(kc * KT + k) * ldb + j0 + n]);
+                const std::uint32_t o = boff<BN>(k, n);
+                bh[o] = static_cast<std::uint8_t>(v >> 8);
+                bl[o] = static_cast<std::uint8_t>(v & 255u);
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&S.full[st]);
+        }
+    }
+
+    const double p = P.pd, pinv = P.pinv;
+    if (warp >= 2) {
+        tc::mbar_wait(&S.done, 0);
+        tc::fence_after();
+        if (tid == 64) WM_DSTAMP(5);
+        // eight warps: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
+        const int lg = warp & 3, half = (warp - 2) >> 2;
+        const std::uint32_t row = lg * 32 + lane;
+        const std::uint32_t lane_off = static_cast<std::uint32_t>(lg * 32) << 16;
+        std::uint16_t* crow = static_cast<std::uint16_t*>(const_cast<void*>(Cd.p)) +
+                              static_cast<std::uint64_t>(i0 + row) * Cd.ld + j0 + half * (BN / 2);
+#pragma unroll
+        for (int q = 0; q < BN / 32; ++q) {
+            std::uint32_t out[16];
+            tmem_cols16<BN>(tbase + lane_off + half * (BN / 2) + q * 16, out, p, pinv);
+            std::uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w[e] = out[2 * e] | (out[2 * e + 1] << 16);
+            reinterpret_cast<uint4*>(crow + q * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(crow + q * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
+        if (tid == 64) WM_DSTAMP(6);
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
+    if (tid == 32) WM_DSTAMP(7);
+}
+
+template <int BN>
+constexpr std::size_t dsmem_bytes() {
+    return sizeof(DSmem<BN>) + 1024;
+}
+
+template <int BN, int BSRC>
+cudaError_t dset_attr() {
+    return cudaFuncSetAttribute(k_gemm_direct<BN, BSRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(dsmem_bytes<BN>()));
+}
+
+template <int BN, int BSRC>
+cudaError_t dlaunch(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1, P.n / BN, P.tiles_m * P.nprod);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = dsmem_bytes<BN>();
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_gemm_direct<BN, BSRC>, P, M);
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_denc = nullptr;
+
+// 3-D byte map over a limb-plane pair: {cols, rows, 2 limbs}
+bool encode_planes(CUtensorMap* map, const GemmSrc& src, std::uint64_t cols, std::uint64_t rows,
+                   std::uint32_t box_c, std::uint32_t box_r, CUtensorMapSwizzle sw) {
+    cuuint64_t dims[3] = {cols, rows, 2};
+    cuuint64_t strides[2] = {src.ld, src.part};
+    cuuint32_t box[3] = {box_c, box_r, 2};
+    cuuint32_t es[3] = {1, 1, 1};
+    return g_denc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(src.p), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool g_direct_ok = false;
+
+}  // namespace
+
+cudaError_t gemm_direct_init() {
+    if (!g_denc) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return e != cudaSuccess ? e : cudaErrorNotSupported;
+        g_denc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cudaError_t e;
+    if ((e = dset_attr<32, 0>()) != cudaSuccess) return e;
+    if ((e = dset_attr<64, 0>()) != cudaSuccess) return e;
+    if ((e = dset_attr<32, 1>()) != cudaSuccess) return e;
+    if ((e = dset_attr<64, 1>()) != cudaSuccess) return e;
+    g_direct_ok = true;
+    return cudaSuccess;
+}
+
+bool gemm_direct_supported(const GemmParams& P, int bn) {
+    bn %= 1000;
+    if (!g_direct_ok || (bn != 32 && bn != 64)) return false;
+    if (P.m % BM || P.n % bn || P.k % KT || P.k > 32768 || P.nprod < 1 || P.nprod > kMaxProducts)
+        return false;
+    for (std::uint32_t i = 0; i < P.nprod; ++i) {
+        if (P.a[i].fmt != 2 || P.c[i].fmt != 1) return false;
+        if (P.b[i].fmt != 2 && P.b[i].fmt != 0) return false;
+    }
+    return true;
+}
+
+bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
+    bn %= 1000;
+    if (!g_denc) return false;
+    std::memset(&M, 0, sizeof(M));
+    const CUtensorMapSwizzle bsw = bn == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+    for (std::uint32_t i = 0; i < P.nprod; ++i) {
+        if (!encode_planes(&M.a[i], P.a[i], P.k, P.m, KT, BM, CU_TENSOR_MAP_SWIZZLE_128B))
+            return false;
+        if (P.b[i].fmt == 2 &&
+            !encode_planes(&M.b[i], P.b[i], P.n, P.k, static_cast<std::uint32_t>(bn), KT, bsw))
+            return false;
+    }
+    return true;
+}
+
+// (BN) for a direct product set: BN 32 unless that leaves the SMs oversubscribed
+int gemm_direct_choose(const GemmParams& P) {
+    const std::uint32_t ctas32 = P.tiles_m * P.nprod * (P.n / 32);
+    return (ctas32 > 2 * 148 && P.n % 64 == 0) ? 64 : 32;
+}
+
+// bn: 32 / 64; + 1000 selects cp.async B loads instead of TMA
+cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s) {
+    switch (bn) {
+        case 32: return dlaunch<32, 0>(P, M, s);
+        case 64: return dlaunch<64, 0>(P, M, s);
+        case 1032: return dlaunch<32, 1>(P, M, s);
+        case 1064: return dlaunch<64, 1>(P, M, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace wm

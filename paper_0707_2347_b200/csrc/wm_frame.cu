@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     // plane values (r, j..j+1) -> 4 bytes at plane + r*pld + j
     auto put = [&](int pl, const double (&v)[2]) {
         if (P.plane[pl])
-            *reinterpret_cast<std::uint32_t*>(P.plane[pl] + r * P.pld[pl] + j) =
+            *reinterpret_cast<std::uint32_t*>(static_cast<std::uint16_t*>(P.plane[pl]) + r * P.pld[pl] + j) =
                 static_cast<std::uint32_t>(v[0]) | (static_cast<std::uint32_t>(v[1]) << 16);
     };
 #pragma unroll
@@ -135,6 +135,86 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
         for (int k = 0; k < 4; ++k)
             *reinterpret_cast<std::uint32_t*>(c11 + 4 * (r * P.C.ld + q + k * c4) + 2 * h) =
                 static_cast<std::uint32_t>(cin[k][0]) | (static_cast<std::uint32_t>(cin[k][1]) << 16);
+    }
+}
+
+// Limb-pair variant for the direct-limb GEMM (wm_direct.cu): one CTA per row r,
+// thread t owns columns j = 2t, 2t+1.  A plane row holds the high bytes of its
+// residues at [0, c) and the low bytes at [c, 2c); every byte a CTA writes lies
+// in row r of its host, and every C_in value of row r is read before the
+// CTA's barrier, so the in-place packing stays race-free.
+__global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams P) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint64_t r = blockIdx.x, j = 2 * threadIdx.x;
+    const double p = P.pd, pinv = P.pinv;
+    double a11[2], a12[2], a21[2], a22[2], b11[2], b12[2], b21[2], b22[2];
+    auto ld2 = [&](const double* ptr, double (&v)[2]) {
+        const double2 x = *reinterpret_cast<const double2*>(ptr);
+        v[0] = x.x;
+        v[1] = x.y;
+    };
+    ld2(P.A.q[0] + r * P.A.ld + j, a11);
+    ld2(P.A.q[1] + r * P.A.ld + j, a12);
+    ld2(P.A.q[2] + r * P.A.ld + j, a21);
+    ld2(P.A.q[3] + r * P.A.ld + j, a22);
+    ld2(P.B.q[0] + r * P.B.ld + j, b11);
+    ld2(P.B.q[1] + r * P.B.ld + j, b12);
+    ld2(P.B.q[2] + r * P.B.ld + j, b21);
+    ld2(P.B.q[3] + r * P.B.ld + j, b22);
+    double cin[4][2];  // [quadrant][column]
+    if (P.beta != 0) {
+        const double be = static_cast<double>(P.beta);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            double v[2];
+            ld2(P.C.q[k] + r * P.C.ld + j, v);
+            cin[k][0] = rmod(be * v[0], p, pinv);
+            cin[k][1] = rmod(be * v[1], p, pinv);
+        }
+    }
+    __syncthreads();  // row r of every host has been read before any of it is overwritten
+    double s[4][2], t[4][2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const double s1 = addm(a21[e], a22[e], p), s2 = subm(s1, a11[e], p);
+        s[0][e] = s1;
+        s[1][e] = s2;
+        s[2][e] = subm(a11[e], a21[e], p);
+        s[3][e] = subm(a12[e], s2, p);
+        const double t1 = subm(b12[e], b11[e], p), t2 = subm(b22[e], t1, p);
+        t[0][e] = t1;
+        t[1][e] = t2;
+        t[2][e] = subm(b22[e], b12[e], p);
+        t[3][e] = subm(t2, b21[e], p);
+    }
+    const std::uint32_t c = P.c;
+    auto put = [&](int pl, const double (&v)[2]) {
+        if (!P.plane[pl]) return;
+        std::uint8_t* row = static_cast<std::uint8_t*>(P.plane[pl]) + r * P.pld[pl];
+        const std::uint32_t x0 = static_cast<std::uint32_t>(v[0]), x1 = static_cast<std::uint32_t>(v[1]);
+        *reinterpret_cast<std::uint16_t*>(row + j) = static_cast<std::uint16_t>((x0 >> 8) | (x1 & 0xFF00u));
+        *reinterpret_cast<std::uint16_t*>(row + c + j) =
+            static_cast<std::uint16_t>((x0 & 255u) | ((x1 & 255u) << 8));
+    };
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        put(PL_S1 + k, s[k]);
+        put(PL_T1 + k, t[k]);
+    }
+    put(PL_A11, a11);
+    put(PL_A12, a12);
+    put(PL_A22, a22);
+    put(PL_B11, b11);
+    put(PL_B21, b21);
+    put(PL_B22, b22);
+    if (P.beta != 0) {
+        std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]) + 4 * (r * P.C.ld + j);
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+            reinterpret_cast<uint2*>(c11)[e] = make_uint2(
+                static_cast<std::uint32_t>(cin[0][e]) | (static_cast<std::uint32_t>(cin[1][e]) << 16),
+                static_cast<std::uint32_t>(cin[2][e]) | (static_cast<std::uint32_t>(cin[3][e]) << 16));
     }
 }
 
@@ -188,10 +268,11 @@ __global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
 }
 
 template <class K, class Prm>
-cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t s) {
+cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t s,
+                       unsigned block = 128) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>((threads + 127) / 128));
-    cfg.blockDim = dim3(128);
+    cfg.gridDim = dim3(static_cast<unsigned>((threads + block - 1) / block));
+    cfg.blockDim = dim3(block);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -204,6 +285,11 @@ cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t
 }  // namespace
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
+    if (P.limbs) {
+        if (P.c > 2048) return cudaErrorInvalidValue;
+        return launch_pdl(k_frame_prep_limbs, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
+                          P.c / 2);
+    }
     return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
 }
 

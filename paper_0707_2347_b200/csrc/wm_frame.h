@@ -19,8 +19,9 @@ enum FramePlane { PL_S1, PL_S2, PL_S3, PL_S4, PL_T1, PL_T2, PL_T3, PL_T4,
 
 struct FramePrepParams {
     FrameQuads A, B, C;
-    std::uint16_t* plane[PL_COUNT];  // nullptr: not materialised (raw blocks only)
-    std::uint64_t pld[PL_COUNT];     // plane leading dimension (uint16 elements)
+    void* plane[PL_COUNT];           // nullptr: not materialised (raw blocks only)
+    std::uint64_t pld[PL_COUNT];     // plane row pitch: uint16 elements, or bytes if limbs
+    std::uint32_t limbs;             // 1: limb-pair planes (hi bytes [0,c), lo [c,2c) per row)
     std::uint32_t c;                 // quadrant size
     std::uint32_t beta;              // accumulate: pack beta*C_in into C11 slots
     double pd, pinv;

@@ -14,8 +14,9 @@ constexpr int kMaxProducts = 7;
 
 struct GemmSrc {
     const void* p;
-    std::uint64_t ld;   // in elements
-    std::uint32_t fmt;  // 0 float64 residues, 1 uint16 residues
+    std::uint64_t ld;    // in elements (fmt 2: row pitch in bytes)
+    std::uint32_t fmt;   // 0 float64 residues, 1 uint16 residues, 2 limb-plane pair
+    std::uint64_t part;  // fmt 2: byte offset of the low-limb plane from the high one
 };
 
 struct GemmParams {
@@ -41,5 +42,13 @@ cudaError_t gemm_tma_init();
 bool gemm_tma_encode(const GemmParams& P, int bn, TmaMaps& M);
 cudaError_t launch_gemm_tma(const GemmParams& P, const TmaMaps& M, int bn, int split,
                             cudaStream_t s);                                  // TMA engine
+
+// Direct-limb engine (wm_direct.cu): operands are limb-plane pairs (fmt 2; B may
+// also be float64), outputs uint16 planes, K a multiple of 128, no K split.
+cudaError_t gemm_direct_init();
+bool gemm_direct_supported(const GemmParams& P, int bn);
+bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M);
+int gemm_direct_choose(const GemmParams& P);
+cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s);
 
 }  // namespace wm

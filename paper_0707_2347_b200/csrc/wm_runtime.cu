@@ -99,6 +99,8 @@ struct wm_ctx {
     int gemm_engine = 0;  // int8 GEMM operand path: 0 cp.async ring, 1 TMA tensor maps
     int frame_cfg = 0;    // measurement: force the frame GEMM tiling (100*BN + split)
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
+    bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
+    bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
     // boundary staging
@@ -276,18 +278,32 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, int force) {
+                 int engine, int force, bool direct) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
     const bool acc = !f.is_zero(op.sb);
     const View& sh = acc ? cq[1] : cq[0];  // S planes host
     const View& th = acc ? cq[2] : cq[1];  // T planes host
-    auto plane = [&](const View& host, int q) {
+    // direct-limb engine: operand planes are limb pairs (hi / lo byte rows) that
+    // the GEMM loads straight into tensor-core layout; prep CTAs own whole rows
+    direct = direct && c <= 2048;
+    // a host row holds four plane rows of 2c bytes; plane q starts at byte 2qc
+    auto plane16 = [&](const View& host, int q) {
         GemmSrc g;
         g.p = reinterpret_cast<std::uint16_t*>(ptr(host)) + q * c;
         g.ld = 4 * host.ld;
         g.fmt = 1;
+        g.part = 0;
+        return g;
+    };
+    auto plane = [&](const View& host, int q) {
+        if (!direct) return plane16(host, q);
+        GemmSrc g;
+        g.p = reinterpret_cast<std::uint8_t*>(ptr(host)) + 2 * q * c;
+        g.ld = 8 * host.ld;
+        g.fmt = 2;
+        g.part = c;
         return g;
     };
     auto f64 = [&](const View& v) {
@@ -295,6 +311,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
         g.p = ptr(v);
         g.ld = v.ld;
         g.fmt = 0;
+        g.part = 0;
         return g;
     };
     const double pd = static_cast<double>(f.p), pinv = 1.0 / static_cast<double>(f.p);
@@ -308,10 +325,13 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     p.fprep.A.ld = op.a.ld;
     p.fprep.B.ld = op.b.ld;
     p.fprep.C.ld = op.d.ld;
-    // raw blocks materialised as uint16 planes where a free host slot exists:
+    p.fprep.limbs = direct ? 1 : 0;
+    // raw blocks materialised as planes where a free host slot exists:
     // plain frames own C21, C22 until the combine; accumulating frames own C22
     // (its beta*C_in is packed away first), a third temporary and the spare
-    // slot of the second product host
+    // slot of the second product host.  Only B22 of a two-temporary
+    // accumulating frame is left in float64 (a B operand: the direct engine
+    // splits it in the GEMM).
     std::vector<std::pair<View, int>> raw_slots;
     if (!acc) {
         for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[2], q});
@@ -326,8 +346,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     for (int i = 0; i < 6; ++i) {
         if (i < static_cast<int>(raw_slots.size())) {
             raw[i] = plane(raw_slots[i].first, raw_slots[i].second);
-            p.fprep.plane[PL_A11 + i] = const_cast<std::uint16_t*>(
-                static_cast<const std::uint16_t*>(raw[i].p));
+            p.fprep.plane[PL_A11 + i] = const_cast<void*>(raw[i].p);
             p.fprep.pld[PL_A11 + i] = raw[i].ld;
         } else {
             raw[i] = f64(raw_view[i]);
@@ -340,8 +359,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
         st[4 + q] = plane(th, q);
     }
     for (int i = 0; i < 8; ++i) {
-        p.fprep.plane[PL_S1 + i] = const_cast<std::uint16_t*>(
-            static_cast<const std::uint16_t*>(st[i].p));
+        p.fprep.plane[PL_S1 + i] = const_cast<void*>(st[i].p);
         p.fprep.pld[PL_S1 + i] = st[i].ld;
     }
     p.fprep.c = static_cast<std::uint32_t>(c);
@@ -354,7 +372,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     g.kind = Step::FGEMM;
     GemmParams& G = g.fgemm;
     // P1 = A11 B11, P2 = A12 B21, P3 = S4 B22, P4 = A22 T4, P5 = S1 T1, P6 = S2 T2, P7 = S3 T3
-    // raw[] = {A11, A12, A22, B11, B21, B22} (uint16 planes or float64 blocks)
+    // raw[] = {A11, A12, A22, B11, B21, B22} (planes or float64 blocks)
     G.a[0] = raw[0]; G.b[0] = raw[3];
     G.a[1] = raw[1]; G.b[1] = raw[4];
     G.a[2] = st[3];  G.b[2] = raw[5];
@@ -362,7 +380,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     G.a[4] = st[0];  G.b[4] = st[4];
     G.a[5] = st[1];  G.b[5] = st[5];
     G.a[6] = st[2];  G.b[6] = st[6];
-    for (int k = 0; k < 7; ++k) G.c[k] = k < 4 ? plane(op.h0, k) : plane(op.h1, k - 4);
+    for (int k = 0; k < 7; ++k) G.c[k] = k < 4 ? plane16(op.h0, k) : plane16(op.h1, k - 4);
     G.m = G.n = G.k = static_cast<std::uint32_t>(c);
     G.nprod = 7;
     G.tiles_m = static_cast<std::uint32_t>(c / 128);
@@ -370,7 +388,18 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     G.beta = 0;
     G.pd = pd;
     G.pinv = pinv;
-    finish_gemm_step(g, engine, force);
+    if (direct) {
+        g.bn = (force >= 1000 && force < 3000) ? force % 1000 + 1000 * (force / 1000 - 1)
+                                                : gemm_direct_choose(G);
+        auto maps = std::make_shared<TmaMaps>();
+        if (!gemm_direct_supported(G, g.bn) || !gemm_direct_encode(G, g.bn, *maps))
+            fail(E_INVALID, "direct-limb frame GEMM: unsupported operands");
+        g.tmaps = maps;
+        g.engine = 2;
+        g.split = 1;
+    } else {
+        finish_gemm_step(g, engine, force);
+    }
     steps.push_back(g);
 
     Step cb{};
@@ -441,7 +470,8 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         flush();
         if (op.kind == OP_FRAME) {
-            lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg);
+            lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
+                        ctx.direct_ok && ctx.direct_frames);
             continue;
         }
         Step s{};
@@ -484,7 +514,8 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
             case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
             case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
             case Step::FGEMM:
-                if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
+                if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
+                else if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
                 else WM_CUDA(launch_gemm_i8(s.fgemm, st));
                 break;
             case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
@@ -521,9 +552,9 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                                     kn = static_cast<std::uint64_t>(G.k) * G.n,
                                     mn = static_cast<std::uint64_t>(G.m) * G.n;
                 for (std::uint32_t i = 0; i < G.nprod; ++i)
-                    r->frame_gemm_bytes += mk * (G.a[i].fmt == 1 ? 2 : 8) +
-                                           kn * (G.b[i].fmt == 1 ? 2 : 8) +
-                                           mn * (G.c[i].fmt == 1 ? 2 : 8);
+                    r->frame_gemm_bytes += mk * (G.a[i].fmt != 0 ? 2 : 8) +
+                                           kn * (G.b[i].fmt != 0 ? 2 : 8) +
+                                           mn * (G.c[i].fmt != 0 ? 2 : 8);
             }
             if (s.kind == Step::FPREP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fprep.c) * s.fprep.c;
@@ -575,7 +606,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -715,6 +746,7 @@ int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out)
         WM_CUDA(leaf_i8_init());
         const bool tma_ok = gemm_tma_init() == cudaSuccess;
         c->gemm_engine = tma_ok ? 1 : 0;
+        c->direct_ok = tma_ok && gemm_direct_init() == cudaSuccess;
         if (stream) {
             c->stream = static_cast<cudaStream_t>(stream);
         } else {
@@ -746,6 +778,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "leaf_kernel") ctx->leaf_kernel = static_cast<int>(value);
         else if (k == "subset") ctx->subset = static_cast<int>(value);
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
+        else if (k == "direct_frames") ctx->direct_frames = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -762,6 +795,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "leaf_kernel") *value = ctx->leaf_kernel;
         else if (k == "subset") *value = ctx->subset;
         else if (k == "fuse_adds") *value = ctx->fuse_adds;
+        else if (k == "direct_frames") *value = ctx->direct_frames;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
@@ -1080,6 +1114,122 @@ int wm_diag_frame_gemm(wm_ctx* ctx, uint32_t c, int cfg, int reps, double* us,
         cudaGraphExecDestroy(ge);
         cudaGraphDestroy(g);
         cudaFree(buf);
+    });
+}
+
+// Diagnostics: seven c x c x c products on random limb planes through the
+// direct-limb engine (product 2 with a float64 B when bconv), checked on the host.
+int wm_diag_direct_check(wm_ctx* ctx, uint32_t c, int bn, int bconv, uint64_t seed,
+                         uint64_t* mismatches, double* us, unsigned long long* trace_out) {
+    return guard([&] {
+        if (!ctx->direct_ok) fail(E_INVALID, "direct engine unavailable");
+        const std::uint64_t p = ctx->f.p, pitch = 2ull * c + 128, cc = static_cast<std::uint64_t>(c) * c;
+        std::vector<std::uint16_t> A(7 * cc), B(7 * cc);
+        std::uint64_t x = seed;
+        auto next = [&]() {
+            std::uint64_t z = (x += 0x9E3779B97F4A7C15ull);
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+            return static_cast<std::uint16_t>((z ^ (z >> 31)) % p);
+        };
+        for (auto& v : A) v = next();
+        for (auto& v : B) v = next();
+        std::vector<std::uint8_t> pa(7 * c * pitch, 0), pb(7 * c * pitch, 0);
+        for (int k = 0; k < 7; ++k)
+            for (std::uint64_t r = 0; r < c; ++r)
+                for (std::uint64_t j = 0; j < c; ++j) {
+                    const std::uint16_t a = A[k * cc + r * c + j], b = B[k * cc + r * c + j];
+                    std::uint8_t* ra = pa.data() + (k * c + r) * pitch;
+                    std::uint8_t* rb = pb.data() + (k * c + r) * pitch;
+                    ra[j] = static_cast<std::uint8_t>(a >> 8);
+                    ra[c + j] = static_cast<std::uint8_t>(a & 255);
+                    rb[j] = static_cast<std::uint8_t>(b >> 8);
+                    rb[c + j] = static_cast<std::uint8_t>(b & 255);
+                }
+        std::vector<double> bf(cc);
+        for (std::uint64_t i = 0; i < cc; ++i) bf[i] = B[2 * cc + i];
+        std::uint8_t *da = nullptr, *db = nullptr;
+        double* dbf = nullptr;
+        std::uint16_t* dout = nullptr;
+        WM_CUDA(cudaMalloc(&da, pa.size()));
+        WM_CUDA(cudaMalloc(&db, pb.size()));
+        WM_CUDA(cudaMalloc(&dbf, cc * sizeof(double)));
+        WM_CUDA(cudaMalloc(&dout, 7 * cc * sizeof(std::uint16_t)));
+        WM_CUDA(cudaMemcpy(da, pa.data(), pa.size(), cudaMemcpyHostToDevice));
+        WM_CUDA(cudaMemcpy(db, pb.data(), pb.size(), cudaMemcpyHostToDevice));
+        WM_CUDA(cudaMemcpy(dbf, bf.data(), cc * sizeof(double), cudaMemcpyHostToDevice));
+        WM_CUDA(cudaMemset(dout, 0xFF, 7 * cc * sizeof(std::uint16_t)));
+        GemmParams G{};
+        for (int k = 0; k < 7; ++k) {
+            G.a[k] = {da + k * c * pitch, pitch, 2, c};
+            G.b[k] = (bconv && k == 2) ? GemmSrc{dbf, c, 0, 0} : GemmSrc{db + k * c * pitch, pitch, 2, c};
+            G.c[k] = {dout + k * cc, c, 1, 0};
+        }
+        G.m = G.n = G.k = c;
+        G.nprod = 7;
+        G.tiles_m = c / 128;
+        G.alpha = 1;
+        G.pd = static_cast<double>(p);
+        G.pinv = 1.0 / G.pd;
+        if (!gemm_direct_supported(G, bn)) fail(E_INVALID, "direct engine: unsupported shape");
+        TmaMaps M;
+        if (!gemm_direct_encode(G, bn, M)) fail(E_INVALID, "direct engine: tensor map encode failed");
+        WM_CUDA(launch_gemm_direct(G, M, bn, ctx->stream));
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        const int reps = 20;
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < reps; ++i) launch_gemm_direct(G, M, bn, ctx->stream);
+        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEventRecord(e0, ctx->stream);
+        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        cudaEventRecord(e1, ctx->stream);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *us = 1000.0 * ms / reps;
+        if (trace_out) {
+            const std::size_t n = static_cast<std::size_t>(G.tiles_m) * 7 * (c / (bn % 1000)) * 16;
+            unsigned long long* dtr = nullptr;
+            WM_CUDA(cudaMalloc(&dtr, n * sizeof(unsigned long long)));
+            WM_CUDA(cudaMemset(dtr, 0, n * sizeof(unsigned long long)));
+            G.trace = dtr;
+            WM_CUDA(launch_gemm_direct(G, M, bn, ctx->stream));
+            WM_CUDA(cudaStreamSynchronize(ctx->stream));
+            G.trace = nullptr;
+            WM_CUDA(cudaMemcpy(trace_out, dtr, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            cudaFree(dtr);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        std::vector<std::uint16_t> out(7 * cc);
+        WM_CUDA(cudaMemcpy(out.data(), dout, out.size() * 2, cudaMemcpyDeviceToHost));
+        cudaFree(da);
+        cudaFree(db);
+        cudaFree(dbf);
+        cudaFree(dout);
+        std::uint64_t bad = 0;
+        std::vector<std::uint64_t> acc(c);
+        for (int k = 0; k < 7; ++k)
+            for (std::uint64_t i = 0; i < c; ++i) {
+                std::fill(acc.begin(), acc.end(), 0);
+                for (std::uint64_t t = 0; t < c; ++t) {
+                    const std::uint64_t a = A[k * cc + i * c + t];
+                    const std::uint16_t* brow = &B[k * cc + t * c];
+                    for (std::uint64_t j = 0; j < c; ++j) acc[j] += a * brow[j];
+                }
+                for (std::uint64_t j = 0; j < c; ++j)
+                    if (out[k * cc + i * c + j] != acc[j] % p) ++bad;
+            }
+        *mismatches = bad;
     });
 }
 

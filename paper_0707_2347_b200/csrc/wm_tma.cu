@@ -24,13 +24,22 @@ namespace cg = cooperative_groups;
 namespace wm {
 namespace {
 
-constexpr int BM = 128, KC = 32, NLIMB = 2, NF = 4;
+constexpr int BM = 128, KC = 32;
+// Staging depth: the MMA commit -> mbarrier round trip is ~0.4 us, so the limb
+// ring must be deep enough that converters never wait on it (2 stages made the
+// K loop latency-bound at ~0.45 us per chunk).
+template <int BN>
+struct Depth {
+    static constexpr int NF = BN == 64 ? 3 : 4;  // TMA staging ring
+    static constexpr int NLIMB = 4;              // converted limb-tile ring
+};
 constexpr int NCONV = 256;
 constexpr int NT = NCONV + 64;  // producer warp + MMA warp + 8 converter warps
 constexpr int A_STAGE = BM * KC * 8;  // 32 KB (float64 worst case)
 
 template <int BN>
 struct Smem {
+    static constexpr int NF = Depth<BN>::NF, NLIMB = Depth<BN>::NLIMB;
     std::uint8_t a[NF][A_STAGE];        // 1024-B aligned (swizzled TMA boxes)
     std::uint8_t b[NF][KC * BN * 8];
     std::uint8_t a_hi[NLIMB][BM * KC];
@@ -167,6 +176,7 @@ __global__ void __launch_bounds__(NT, 1)
     const std::uint32_t base = tc::smem_u32(smem_raw);
     Smem<BN>& S = *reinterpret_cast<Smem<BN>*>(smem_raw + ((1024 - (base & 1023)) & 1023));
     constexpr std::uint32_t TCOLS = BN == 32 ? 128 : 256;
+    constexpr int NF = Depth<BN>::NF, NLIMB = Depth<BN>::NLIMB;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ks = SPLIT > 1 ? static_cast<int>(blockIdx.x) : 0;
     const int prod = static_cast<int>(blockIdx.z / P.tiles_m);
@@ -228,6 +238,7 @@ __global__ void __launch_bounds__(NT, 1)
             const int ls = kc % NLIMB;
             tc::mbar_wait(&S.lfull[ls], (kc / NLIMB) & 1);
             tc::fence_after();
+            if (lane == 0 && kc == 4) WM_STAMP(15);
             if (lane == 0) {
                 const std::uint64_t ah = tc::smem_desc(tc::smem_u32(S.a_hi[ls]), 128, 256);
                 const std::uint64_t al = tc::smem_desc(tc::smem_u32(S.a_lo[ls]), 128, 256);
@@ -249,8 +260,12 @@ __global__ void __launch_bounds__(NT, 1)
             const int st = kc % NF, ls = kc % NLIMB;
             tc::mbar_wait(&S.full[st], (kc / NF) & 1);
             if (ct == 0 && kc == 0) WM_STAMP(3);
+            if (ct == 0 && kc == 2) WM_STAMP(11);
+            if (ct == 0 && kc == 5) WM_STAMP(13);
             if (kc >= static_cast<std::uint32_t>(NLIMB))
                 tc::mbar_wait(&S.lempty[ls], ((kc / NLIMB) - 1) & 1);
+            if (ct == 0 && kc == 2) WM_STAMP(12);
+            if (ct == 0 && kc == 5) WM_STAMP(14);
             convert_a(S.a[st], S.a_hi[ls], S.a_lo[ls], ct, a16);
             convert_b<BN>(S.b[st], S.b_hi[ls], S.b_lo[ls], ct, b16);
             tc::fence_proxy_async();

@@ -15,23 +15,24 @@ L.wm_diag_frame_gemm.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int,
                                  C.POINTER(C.c_double), C.c_void_p, C.POINTER(C.c_int)]
 ctx = W.Context.get()
 out = {}
-for c in (128, 256, 512):
-    for cfg in (0, 3201, 3202, 3204, 6401, 6402, 6404):
+for c in (256,):
+    for cfg in (0, 3201):
         us = C.c_double()
         n = C.c_int()
         rc = L.wm_diag_frame_gemm(ctx.h, c, cfg, 50, C.byref(us), None, C.byref(n))
         out[f"c{c}_cfg{cfg}"] = (round(us.value, 2), n.value) if rc == 0 else _lib.last_error()
-    # trace the automatic configuration
+    # trace the no-split BN32 configuration (8 chunks per CTA at c=256)
     us = C.c_double()
     n = C.c_int()
-    L.wm_diag_frame_gemm(ctx.h, c, 0, 5, C.byref(us), None, C.byref(n))
+    L.wm_diag_frame_gemm(ctx.h, c, 3201, 5, C.byref(us), None, C.byref(n))
     tr = np.zeros(n.value * 16, dtype=np.uint64)
-    L.wm_diag_frame_gemm(ctx.h, c, 0, 5, C.byref(us), tr.ctypes.data, C.byref(n))
+    L.wm_diag_frame_gemm(ctx.h, c, 3201, 5, C.byref(us), tr.ctypes.data, C.byref(n))
     tr = tr.reshape(n.value, 16).astype(np.int64)
     t0 = tr[:, 0].min()
     phases = {}
     names = ["start", "init", "gdc_wait", "first_chunk", "loop_end", "mma_done", "part_written",
-             "cluster_sync1", "reduced", "pre_dealloc", "end"]
+             "cluster_sync1", "reduced", "pre_dealloc", "end", "full2", "lempty2",
+             "full5", "lempty5", "mma4_issue"]
     for i, nm in enumerate(names):
         col = tr[:, i]
         col = col[col > 0]

@@ -43,12 +43,13 @@ def golden():
 
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
                         dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
-                        dict(gemm_engine=0)],
-                ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync"])
+                        dict(gemm_engine=0), dict(direct_frames=0)],
+                ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync", "convert-frames"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
-                                              "leaf_kernel", "fuse_adds", "gemm_engine")}
+                                              "leaf_kernel", "fuse_adds", "gemm_engine",
+                                              "direct_frames")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
@@ -141,13 +142,14 @@ def test_midsize_vs_oracle(W, O, v, options):
 CFG = json.load(open(os.path.join(GOLD, "config_hashes.json")))
 
 
-@pytest.mark.parametrize("fused", [0, 1], ids=["unfused", "fused"])
+@pytest.mark.parametrize("fused", [0, 1, 2], ids=["unfused", "fused", "fused-convert"])
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_config_full_size_hash(W, name, fused):
     if name not in CFG:
         pytest.skip("hash not generated")
     ctx = W.Context.get()
-    ctx.set_option("fuse_frames", fused)
+    ctx.set_option("fuse_frames", 1 if fused else 0)
+    ctx.set_option("direct_frames", 1 if fused != 2 else 0)
     ctx.set_option("leaf_kernel", 2)
     c = CFG[name]
     want = c["appendix_a"]
@@ -158,6 +160,26 @@ def test_config_full_size_hash(W, name, fused):
     e = W.expected_costs(c["variant"], c["m"], c["k"], c["n"], c["cutoff"])
     assert rep.peak_extra_words == e.peak_extra_words
     assert rep.peak_extra_bytes == 8 * e.peak_extra_words
+    ctx.set_option("direct_frames", 1)
+
+
+@pytest.mark.parametrize("c", [128, 256, 512])
+@pytest.mark.parametrize("bn", [32, 64, 1032])
+@pytest.mark.parametrize("bconv", [0, 1], ids=["planes", "f64-B"])
+def test_direct_limb_gemm(W, c, bn, bconv):
+    """Seven-product direct-limb frame GEMM on random limb planes (one product
+    with a float64 B), every residue checked on the host (wm_diag_direct_check)."""
+    import ctypes as C
+    from paper_0707_2347_b200 import _lib
+    L = _lib.lib()
+    f = L.wm_diag_direct_check
+    f.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int, C.c_uint64,
+                  C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.c_void_p]
+    f.restype = C.c_int
+    bad, us = C.c_uint64(), C.c_double()
+    rc = f(W.Context.get().h, c, bn, bconv, 1000 + c + bn, C.byref(bad), C.byref(us), None)
+    assert rc == 0, _lib.last_error() if hasattr(_lib, "last_error") else rc
+    assert bad.value == 0
 
 
 def test_host_u32_end_to_end(W, O):
