@@ -233,6 +233,9 @@ def main():
         ctx.set_option("frame_cfg", int(os.environ["WM_FRAME_CFG"]))
     if os.environ.get("WM_GEMM_ENGINE"):
         ctx.set_option("gemm_engine", int(os.environ["WM_GEMM_ENGINE"]))
+    for kv in filter(None, os.environ.get("WM_OPTS", "").split(",")):  # measurement sweeps
+        opt_name, opt_val = kv.split("=")
+        ctx.set_option(opt_name.strip(), int(opt_val))
 
     def reset_inputs():
         A.fill_random(cfg["seed"])

@@ -31,9 +31,75 @@ __global__ void k_stream(const double2* __restrict__ src, double2* __restrict__ 
     if (!write && acc.x == 12345.678) dst[0] = acc;
 }
 
+// one chained "prep-like" step: every thread reads `nin` 16-B words (strided by
+// the grid) and writes `nout` 16-B words
+__global__ void k_chain(const double2* __restrict__ src, double2* __restrict__ dst, int nin,
+                        int nout, std::uint64_t stride) {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    double2 acc = make_double2(0, 0);
+    for (int i = 0; i < nin; ++i) {
+        const double2 v = src[t + i * stride];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+    for (int i = 0; i < nout; ++i) dst[t + i * stride] = make_double2(acc.x + i, acc.y);
+}
+
 }  // namespace
 
 extern "C" {
+
+// Microseconds per kernel of a PDL chain of `n` k_chain launches (graph replay):
+// `threads` threads each reading nin and writing nout 16-B words, rotating over
+// `nbuf` buffer pairs (L2-resident when small).
+int wm_diag_chain(int threads, int block, int nin, int nout, int n, int nbuf, double* us) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 12;
+    const std::uint64_t stride = static_cast<std::uint64_t>(threads);
+    const std::uint64_t words = stride * (nin > nout ? nin : nout);
+    double2* buf = nullptr;
+    if (cudaMalloc(&buf, 2 * nbuf * words * sizeof(double2)) != cudaSuccess) return 12;
+    cudaMemset(buf, 0, 2 * nbuf * words * sizeof(double2));
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    for (int i = 0; i < n; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((threads + block - 1) / block);
+        cfg.blockDim = dim3(block);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const int b = i % nbuf;
+        cudaLaunchKernelEx(&cfg, k_chain, buf + 2 * b * words, buf + (2 * b + 1) * words, nin, nout,
+                           stride);
+    }
+    cudaStreamEndCapture(s, &g);
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) return 12;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaGraphLaunch(ge, s);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(e0, s);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *us = 1000.0 * ms / (reps * n);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(buf);
+    cudaStreamDestroy(s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 12;
+}
 
 // Average microseconds per kernel of `n` dependent single-CTA kernels replayed as
 // one CUDA graph (pdl=1: launched with programmatic stream serialization).

@@ -32,6 +32,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include "wm_launch.h"
 #include "wm_gemm.h"
 #include "wm_tc.h"
 
@@ -39,6 +40,8 @@ namespace wm {
 namespace {
 
 constexpr int BM = 128, KT = 128, NS = 4;
+// A tiles are K-major with a KT-byte swizzle span (SW64 for KT = 64)
+constexpr std::uint64_t A_LAYOUT = KT == 128 ? 2 : 4;  // UMMA SWIZZLE_128B / SWIZZLE_64B
 constexpr int NEPI = 256;           // eight epilogue / B-loader warps
 constexpr int NT = 64 + NEPI;      // + TMA producer warp + MMA warp
 constexpr int A_PART = BM * KT;  // 16 KB per limb
@@ -46,7 +49,7 @@ constexpr int A_PART = BM * KT;  // 16 KB per limb
 template <int BN>
 struct DCfg {
     static constexpr int B_PART = KT * BN;
-    static constexpr int STAGE = 2 * A_PART + 2 * B_PART;  // 40 KB (BN 32) / 48 KB (BN 64)
+    static constexpr int STAGE = 2 * A_PART + 2 * B_PART;  // 20 KB (BN 32) / 24 KB (BN 64)
     static constexpr std::uint32_t TCOLS = BN == 32 ? 128 : 256;
     // UMMA layout type of the MN-major B tile (swizzle span = BN bytes)
     static constexpr std::uint64_t B_LAYOUT = BN == 32 ? 6 : 4;  // SWIZZLE_32B / SWIZZLE_64B
@@ -95,6 +98,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// multicast variant: the box lands at the same offset in every CTA of `mask`
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int x, int y,
+                                               int z, std::uint64_t* mbar, std::uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(tc::smem_u32(dst)),
+        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(z),
+        "r"(tc::smem_u32(mbar)), "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ std::uint32_t cluster_rank() {
+    std::uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
 // byte offset of B element (k, n) in a BN-byte-swizzled MN-major limb tile
 template <int BN>
 __device__ __forceinline__ std::uint32_t boff(std::uint32_t k, std::uint32_t n) {
@@ -110,7 +134,8 @@ __device__ __forceinline__ double u2d(std::uint32_t u) {
 }
 
 // 16 accumulator columns of one TMEM lane: D_h = A_h [B_h | B_l] at [0, 2BN),
-// D_l = A_l [B_h | B_l] at [2BN, 4BN); v = 2^16 hh + 2^8 (hl + lh) + ll < 2^50.
+// D_l = A_l [B_h | B_l] at [2BN, 4BN); v = 2^16 hh + 2^8 (hl + lh) + ll < 2^48
+// (each accumulator <= k 255^2 < 2^31 for k <= 32768, so hl + lh fits 32 bits).
 // The residue r = v - q p uses q = rint(v / p) from a magic-constant FMA and one
 // sign fix, and leaves as an integer through the same 2^52 trick: the epilogue
 // runs on the float64 FMA pipe only (no I2F / F2I / FRND, which are 4-16x slower).
@@ -126,10 +151,14 @@ __device__ __forceinline__ void tmem_cols16(std::uint32_t taddr, std::uint32_t (
     tc::tmem_wait_ld();
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-        const double x = u2d(hl[e]) + u2d(lh[e]);
-        const double v = fma(u2d(hh[e]), 65536.0, fma(x, 256.0, u2d(ll[e])));
-        const double q = fma(v, pinv, kMagic) - kMagic;
-        double r = fma(-q, p, v);  // exact, |r| <= p/2 + 1
+        // v < 2^48 assembled in integer registers, then one exact 2^52 move to float64
+        const std::uint64_t v = (static_cast<std::uint64_t>(hh[e]) << 16) +
+                                (static_cast<std::uint64_t>(hl[e] + lh[e]) << 8) + ll[e];
+        const double d = __hiloint2double(0x43300000 | static_cast<int>(v >> 32),
+                                          static_cast<int>(v & 0xFFFFFFFFu)) -
+                         4503599627370496.0;
+        const double q = fma(d, pinv, kMagic) - kMagic;
+        double r = fma(-q, p, d);  // exact, |r| <= p/2 + 1
         r = r < 0.0 ? r + p : r;
         out[e] = static_cast<std::uint32_t>(__double2loint(r + 4503599627370496.0));
     }
@@ -172,6 +201,15 @@ __global__ void __launch_bounds__(NT, 1)
     const bool bconv = P.b[prod].fmt == 0;  // float64 B: split by the epilogue warps
     const bool blsu = !bconv && BSRC == 1;
     const GemmSrc Cd = P.c[prod];
+    // TMA multicast: a cluster spans mc_n N tiles x mc_m M tiles of one product;
+    // each CTA fetches 1/mc_n of the A rows (shared along N) and 1/mc_m of the
+    // B K-rows (shared along M) and multicasts them, so one SM's TMA unit walks
+    // 192 instead of 512 box rows per stage.  Only used when no stage is reused
+    // (nk <= NS), so no cross-CTA "empty" handshake is needed.
+    const std::uint32_t mcn = P.mc_n, mcm = P.mc_m;
+    const bool mc = mcn * mcm > 1;
+    const std::uint32_t crank = mc ? cluster_rank() : 0;
+    const std::uint32_t cy = crank % mcn, cz = crank / mcn;
 
     if (tid == 32) WM_DSTAMP(0);
     if (warp == 0) tc::tmem_alloc(&S.tmem_base, C::TCOLS);
@@ -186,6 +224,7 @@ __global__ void __launch_bounds__(NT, 1)
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    if (mc) cluster_sync_all();  // peers' barriers are initialised before any multicast lands
     const std::uint32_t tbase = S.tmem_base;
     if (tid == 32) WM_DSTAMP(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -202,10 +241,25 @@ __global__ void __launch_bounds__(NT, 1)
                     tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
                 tc::mbar_arrive_expect_tx(&S.full[st], bytes);
                 const int k0 = static_cast<int>(kc * KT);
-                tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
-                if (btma)
-                    tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0, 0,
-                                &S.full[st]);
+                if (!mc) {
+                    tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
+                    if (btma)
+                        tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0,
+                                    0, &S.full[st]);
+                } else {
+                    const std::uint32_t ra = BM / mcn, rb = KT / mcm;
+                    const std::uint16_t amask = static_cast<std::uint16_t>(((1u << mcn) - 1) << (cz * mcn));
+                    std::uint16_t bmask = 0;
+                    for (std::uint32_t z = 0; z < mcm; ++z) bmask |= static_cast<std::uint16_t>(1u << (cy + z * mcn));
+                    for (int limb = 0; limb < 2; ++limb) {
+                        tma_load_3d_mc(S.stage[st] + limb * A_PART + cy * ra * KT, &M.a[prod], k0,
+                                       static_cast<int>(i0 + cy * ra), limb, &S.full[st], amask);
+                        if (btma)
+                            tma_load_3d_mc(S.stage[st] + 2 * A_PART + limb * C::B_PART + cz * rb * BN,
+                                           &M.b[prod], static_cast<int>(j0),
+                                           static_cast<int>(k0 + cz * rb), limb, &S.full[st], bmask);
+                    }
+                }
             }
         }
     } else if (warp == 1) {
@@ -223,9 +277,9 @@ __global__ void __launch_bounds__(NT, 1)
                 const std::uint32_t sb = sa + 2 * A_PART;
 #pragma unroll
                 for (int s = 0; s < KT / 32; ++s) {
-                    // A: K-major SW128, K step = 32 bytes inside the 128-B swizzle row
-                    const std::uint64_t ah = sdesc(sa + s * 32, 16, 1024, 2);
-                    const std::uint64_t al = sdesc(sa + A_PART + s * 32, 16, 1024, 2);
+                    // A: K-major, KT-byte swizzle; K step = 32 bytes inside the swizzled row
+                    const std::uint64_t ah = sdesc(sa + s * 32, 16, 8 * KT, A_LAYOUT);
+                    const std::uint64_t al = sdesc(sa + A_PART + s * 32, 16, 8 * KT, A_LAYOUT);
                     // B: MN-major, BN-byte swizzle, K step = 32 rows
                     const std::uint64_t b = sdesc(sb + s * 32 * BN, C::B_PART, 8 * BN, C::B_LAYOUT);
                     const bool acc = kc > 0 || s > 0;
@@ -310,6 +364,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
     tc::fence_before();
     __syncthreads();
+    if (mc) cluster_sync_all();  // no CTA leaves while a peer's multicast may still target it
     if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
     if (tid == 32) WM_DSTAMP(7);
 }
@@ -332,22 +387,31 @@ cudaError_t dlaunch(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = dsmem_bytes<BN>();
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    int na = 1;
+    if (P.mc_n * P.mc_m > 1) {
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 1;
+        attr[1].val.clusterDim.y = P.mc_n;
+        attr[1].val.clusterDim.z = P.mc_m;
+        na = 2;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, k_gemm_direct<BN, BSRC>, P, M);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_denc = nullptr;
 
-// 3-D byte map over a limb-plane pair: {cols, rows, 2 limbs}
+// 3-D byte map over a limb-plane pair: {cols, rows, 2 limbs}; box_l limbs per box
 bool encode_planes(CUtensorMap* map, const GemmSrc& src, std::uint64_t cols, std::uint64_t rows,
-                   std::uint32_t box_c, std::uint32_t box_r, CUtensorMapSwizzle sw) {
+                   std::uint32_t box_c, std::uint32_t box_r, CUtensorMapSwizzle sw,
+                   std::uint32_t box_l = 2) {
     cuuint64_t dims[3] = {cols, rows, 2};
     cuuint64_t strides[2] = {src.ld, src.part};
-    cuuint32_t box[3] = {box_c, box_r, 2};
+    cuuint32_t box[3] = {box_c, box_r, box_l};
     cuuint32_t es[3] = {1, 1, 1};
     return g_denc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(src.p), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -393,11 +457,14 @@ bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
     if (!g_denc) return false;
     std::memset(&M, 0, sizeof(M));
     const CUtensorMapSwizzle bsw = bn == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const bool mc = P.mc_n * P.mc_m > 1;
+    const std::uint32_t mn = mc ? P.mc_n : 1, mm = mc ? P.mc_m : 1, bl = mc ? 1 : 2;
     for (std::uint32_t i = 0; i < P.nprod; ++i) {
-        if (!encode_planes(&M.a[i], P.a[i], P.k, P.m, KT, BM, CU_TENSOR_MAP_SWIZZLE_128B))
+        if (!encode_planes(&M.a[i], P.a[i], P.k, P.m, KT, BM / mn,
+                           KT == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, bl))
             return false;
         if (P.b[i].fmt == 2 &&
-            !encode_planes(&M.b[i], P.b[i], P.n, P.k, static_cast<std::uint32_t>(bn), KT, bsw))
+            !encode_planes(&M.b[i], P.b[i], P.n, P.k, static_cast<std::uint32_t>(bn), KT / mm, bsw, bl))
             return false;
     }
     return true;
@@ -407,6 +474,17 @@ bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
 int gemm_direct_choose(const GemmParams& P) {
     const std::uint32_t ctas32 = P.tiles_m * P.nprod * (P.n / 32);
     return (ctas32 > 2 * 148 && P.n % 64 == 0) ? 64 : 32;
+}
+
+// Multicast cluster for a direct launch (sets P.mc_n / P.mc_m): up to 4 N tiles
+// x 2 M tiles of one product, only when every K stage has its own ring slot.
+void gemm_direct_cluster(GemmParams& P, int bn, bool enable) {
+    bn %= 1000;
+    P.mc_n = P.mc_m = 1;
+    if (!enable || P.k / KT > static_cast<std::uint32_t>(NS)) return;
+    const std::uint32_t nt = P.n / bn;
+    P.mc_n = nt % 4 == 0 ? 4 : nt % 2 == 0 ? 2 : 1;
+    P.mc_m = P.tiles_m % 2 == 0 ? 2 : 1;
 }
 
 // bn: 32 / 64; + 1000 selects cp.async B loads instead of TMA

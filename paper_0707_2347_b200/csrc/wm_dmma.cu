@@ -12,6 +12,7 @@
 // dimension are handled.
 #include <cstdint>
 
+#include "wm_launch.h"
 #include "wm_device.h"
 
 namespace wm {
@@ -147,7 +148,7 @@ cudaError_t launch_leaf_dmma(const MulParams& P, bool real, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (real) return cudaLaunchKernelEx(&cfg, k_leaf_dmma<true>, P);

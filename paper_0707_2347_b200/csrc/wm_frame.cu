@@ -22,6 +22,7 @@
 // packing is race-free.
 #include <cstdint>
 
+#include "wm_launch.h"
 #include "wm_frame.h"
 
 namespace wm {
@@ -276,7 +277,7 @@ cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, P);

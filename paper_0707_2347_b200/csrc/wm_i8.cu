@@ -32,6 +32,7 @@
 
 #include <cstdint>
 
+#include "wm_launch.h"
 #include "wm_device.h"
 #include "wm_gemm.h"
 #include "wm_tc.h"
@@ -389,7 +390,7 @@ cudaError_t launch_cfg(const GemmParams& P, cudaStream_t s) {
     cudaLaunchAttribute attr[2];
     int na = 0;
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    attr[na].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     ++na;
     if (SPLIT > 1) {
         attr[na].id = cudaLaunchAttributeClusterDimension;

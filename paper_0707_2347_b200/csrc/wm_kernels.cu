@@ -10,10 +10,13 @@
 // correction and the general sa*a + sb*b (< 2^33) one floor-based reduction.
 #include <cstdint>
 
+#include "wm_launch.h"
 #include "wm_device.h"
 #include "wm_fused.h"
 
 namespace wm {
+
+bool g_pdl = true;
 namespace {
 
 template <bool REAL>
@@ -207,7 +210,7 @@ cudaError_t launch_addsub(const AddBatch& b, bool real, unsigned blocks, cudaStr
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
 #define WM_ADD_LAUNCH(I)                                                       \
@@ -229,7 +232,7 @@ cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaSt
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G);

@@ -24,6 +24,7 @@
 #include "wm_frame.h"
 #include "wm_fused.h"
 #include "wm_gemm.h"
+#include "wm_launch.h"
 #include "wm_planner.h"
 
 namespace wm {
@@ -68,11 +69,37 @@ struct Step {
     int engine = 0;         // int8 GEMM: 0 cp.async, 1 TMA
     int bn = 32, split = 1;
     std::shared_ptr<TmaMaps> tmaps;
+    // memory the launch reads / writes (dependency analysis for concurrent issue)
+    std::vector<View> rd, wr;
 };
 
+// Read / write sets of one planned operation (a fused frame also writes the
+// blocks hosting its planes).
+void op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) {
+    wr.push_back(o.d);
+    rd.push_back(o.a);
+    if (o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) rd.push_back(o.b);
+    if (o.kind == OP_MUL || o.kind == OP_FRAME) rd.push_back(o.d);
+    if (o.kind == OP_FRAME)
+        for (const View* h : {&o.h0, &o.h1, &o.h2})
+            if (h->rows) wr.push_back(*h);
+}
+
+bool sets_conflict(const Step& a, const Step& b) {
+    auto hit = [](const std::vector<View>& x, const std::vector<View>& y) {
+        for (const View& u : x)
+            for (const View& v : y)
+                if (u.phys_overlaps(v)) return true;
+        return false;
+    };
+    return hit(a.wr, b.rd) || hit(a.wr, b.wr) || hit(a.rd, b.wr);
+}
+
+struct DagPlan;
 struct CachedPlan {
     Plan plan;
     std::vector<Step> steps;
+    std::shared_ptr<DagPlan> dag;  // concurrent issue plan (lanes option)
     double* arena = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
@@ -84,6 +111,21 @@ struct CachedPlan {
 };
 
 }  // namespace
+
+constexpr int kLanes = 4;
+
+struct Lanes {
+    cudaStream_t s[kLanes] = {};
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t join[kLanes] = {};
+    ~Lanes() {
+        for (int l = 1; l < kLanes; ++l)
+            if (s[l]) cudaStreamDestroy(s[l]);
+        for (auto e : ev) cudaEventDestroy(e);
+        for (auto e : join)
+            if (e) cudaEventDestroy(e);
+    }
+};
 
 struct wm_ctx {
     int device = 0;
@@ -101,6 +143,9 @@ struct wm_ctx {
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
+    bool dag = true;            // concurrent issue over kLanes streams (dependency DAG)
+    bool multicast = true;      // direct frame GEMM: TMA multicast across N / M tile clusters
+    Lanes lanes;
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
     // boundary staging
@@ -278,7 +323,7 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, int force, bool direct) {
+                 int engine, int force, bool direct, bool multicast) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
@@ -392,6 +437,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
         g.bn = (force >= 1000 && force < 3000) ? force % 1000 + 1000 * (force / 1000 - 1)
                                                 : gemm_direct_choose(G);
         auto maps = std::make_shared<TmaMaps>();
+        gemm_direct_cluster(G, g.bn, multicast);
         if (!gemm_direct_supported(G, g.bn) || !gemm_direct_encode(G, g.bn, *maps))
             fail(E_INVALID, "direct-limb frame GEMM: unsupported operands");
         g.tmaps = maps;
@@ -436,6 +482,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             t.blk0 = blk;
             blk += item_blocks(t);
             s.add.it[s.add.n++] = t;
+            op_sets(*op, s.rd, s.wr);
         }
         s.blocks = blk;
         steps.push_back(s);
@@ -457,6 +504,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             Step gs{};
             if (g >= 0 && try_group(plan, oi, g, base, gs)) {
                 flush();
+                for (int j = 0; j < fused::kGroups[g].nins; ++j) op_sets(plan.ops[oi + j], gs.rd, gs.wr);
                 steps.push_back(gs);
                 oi += fused::kGroups[g].nins - 1;
                 continue;
@@ -470,8 +518,10 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         flush();
         if (op.kind == OP_FRAME) {
+            const std::size_t first = steps.size();
             lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
-                        ctx.direct_ok && ctx.direct_frames);
+                        ctx.direct_ok && ctx.direct_frames, ctx.multicast);
+            for (std::size_t j = first; j < steps.size(); ++j) op_sets(op, steps[j].rd, steps[j].wr);
             continue;
         }
         Step s{};
@@ -485,10 +535,34 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 finish_gemm_step(s, ctx.gemm_engine);
             }
         }
+        op_sets(op, s.rd, s.wr);
         steps.push_back(s);
     }
     flush();
     return steps;
+}
+
+void issue_one(const Step& s, bool real, cudaStream_t st) {
+    switch (s.kind) {
+        case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
+        case Step::MUL:
+            if (s.leaf == 1) {
+                if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
+                else WM_CUDA(launch_gemm_i8(s.fgemm, st));
+            } else {
+                WM_CUDA(launch_leaf_dmma(s.mul, real, st));
+            }
+            break;
+        case Step::FRAME: break;
+        case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
+        case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
+        case Step::FGEMM:
+            if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
+            else if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
+            else WM_CUDA(launch_gemm_i8(s.fgemm, st));
+            break;
+        case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
+    }
 }
 
 void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subset = 0) {
@@ -500,27 +574,114 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
         if (subset == 4 && s.kind != Step::FPREP) continue;
         if (subset == 5 && s.kind != Step::FGEMM) continue;
         if (subset == 6 && s.kind != Step::FCOMB) continue;
-        switch (s.kind) {
-            case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
-            case Step::MUL:
-                if (s.leaf == 1) {
-                    if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
-                    else WM_CUDA(launch_gemm_i8(s.fgemm, st));
-                } else {
-                    WM_CUDA(launch_leaf_dmma(s.mul, real, st));
-                }
-                break;
-            case Step::FRAME: break;
-            case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
-            case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
-            case Step::FGEMM:
-                if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
-                else if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
-                else WM_CUDA(launch_gemm_i8(s.fgemm, st));
-                break;
-            case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
+        issue_one(s, real, st);
+    }
+}
+
+// Concurrent issue.  The memory-lean schedules are mostly a chain, but
+// independent launches exist (about 1.2-1.5x of slack on the configurations'
+// operation DAGs, wm_diag_plan_dag), and every launch here is latency-bound, so
+// running them side by side pays.  Each step goes to one of kLanes streams:
+// the lane of its latest conflicting predecessor (stream order then covers that
+// edge), other conflicting lanes are joined through events.  Dependencies are
+// exact within an epoch of kEpoch steps; at epoch boundaries every lane joins.
+struct DagPlan {
+    std::vector<int> lane;                // per step
+    std::vector<std::vector<int>> waits;  // per step: steps (other lanes) to wait for
+    std::vector<char> record;             // per step: an event is recorded after it
+    std::vector<char> epoch_end;          // per step: all lanes join after it
+};
+
+constexpr int kEpoch = 512;
+
+DagPlan plan_dag(const std::vector<Step>& steps) {
+    const int n = static_cast<int>(steps.size());
+    DagPlan d;
+    d.lane.assign(n, 0);
+    d.waits.assign(n, {});
+    d.record.assign(n, 0);
+    d.epoch_end.assign(n, 0);
+    int epoch0 = 0;
+    int last_on[kLanes];
+    int synced[kLanes][kLanes];  // synced[a][b]: latest step of lane b that lane a waited for
+    for (int j = 0; j < n; ++j) {
+        if (j - epoch0 == kEpoch) {
+            d.epoch_end[j - 1] = 1;
+            epoch0 = j;
+        }
+        if (j == epoch0)
+            for (int l = 0; l < kLanes; ++l) {
+                last_on[l] = -1;
+                for (int m = 0; m < kLanes; ++m) synced[l][m] = -1;
+            }
+        // latest conflicting step per lane (earlier ones on a lane are implied)
+        int dep[kLanes];
+        for (int l = 0; l < kLanes; ++l) dep[l] = -1;
+        int open = kLanes;
+        for (int i = j - 1; i >= epoch0 && open > 0; --i) {
+            const int l = d.lane[i];
+            if (dep[l] >= 0) continue;
+            if (sets_conflict(steps[i], steps[j])) {
+                dep[l] = i;
+                --open;
+            }
+        }
+        int best = -1;
+        for (int l = 0; l < kLanes; ++l)
+            if (dep[l] >= 0 && (best < 0 || dep[l] > dep[best])) best = l;
+        if (best < 0) {
+            // independent of the epoch so far: the least recently used lane
+            best = 0;
+            for (int l = 1; l < kLanes; ++l)
+                if (last_on[l] < last_on[best]) best = l;
+        }
+        d.lane[j] = best;
+        for (int l = 0; l < kLanes; ++l)
+            if (l != best && dep[l] > synced[best][l]) {
+                d.waits[j].push_back(dep[l]);
+                d.record[dep[l]] = 1;
+                synced[best][l] = dep[l];
+            }
+        last_on[best] = j;
+    }
+    return d;
+}
+
+void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cudaStream_t main,
+               Lanes& L) {
+    const int n = static_cast<int>(steps.size());
+    L.s[0] = main;
+    for (int l = 1; l < kLanes; ++l)
+        if (!L.s[l]) WM_CUDA(cudaStreamCreateWithFlags(&L.s[l], cudaStreamNonBlocking));
+    for (int l = 0; l < kLanes; ++l)
+        if (!L.join[l]) WM_CUDA(cudaEventCreateWithFlags(&L.join[l], cudaEventDisableTiming));
+    while (static_cast<int>(L.ev.size()) < n) {
+        cudaEvent_t e;
+        WM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        L.ev.push_back(e);
+    }
+    auto fork = [&]() {  // every lane starts after what is already on the main stream
+        WM_CUDA(cudaEventRecord(L.join[0], main));
+        for (int l = 1; l < kLanes; ++l) WM_CUDA(cudaStreamWaitEvent(L.s[l], L.join[0], 0));
+    };
+    auto join = [&]() {  // the main stream continues after every lane
+        for (int l = 1; l < kLanes; ++l) {
+            WM_CUDA(cudaEventRecord(L.join[l], L.s[l]));
+            WM_CUDA(cudaStreamWaitEvent(main, L.join[l], 0));
+        }
+    };
+    fork();
+    for (int j = 0; j < n; ++j) {
+        cudaStream_t st = L.s[d.lane[j]];
+        for (int i : d.waits[j]) WM_CUDA(cudaStreamWaitEvent(st, L.ev[i], 0));
+        issue_one(steps[j], real, st);
+        if (d.record[j]) WM_CUDA(cudaEventRecord(L.ev[j], st));
+        if (d.epoch_end[j]) {
+            join();
+            fork();
         }
     }
+    join();
 }
 
 void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r) {
@@ -606,7 +767,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -629,11 +790,17 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
         cp = ctx->cache.front().second.get();
     }
+    const bool dag = ctx->dag && ctx->subset == 0 && cp->steps.size() > 1;
+    if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps));
+    auto go = [&]() {
+        if (dag) issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes);
+        else issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
+    };
     if (ctx->graphs && cp->steps.size() > 1) {
         if (!cp->exec) {
             WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             try {
-                issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
+                go();
             } catch (...) {
                 cudaGraph_t g = nullptr;
                 cudaStreamEndCapture(ctx->stream, &g);
@@ -645,7 +812,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         }
         WM_CUDA(cudaGraphLaunch(cp->exec, ctx->stream));
     } else {
-        issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
+        go();
     }
     fill_report(cp->plan, &cp->steps, rep);
 }
@@ -779,6 +946,9 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "subset") ctx->subset = static_cast<int>(value);
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
         else if (k == "direct_frames") ctx->direct_frames = value != 0;
+        else if (k == "dag") ctx->dag = value != 0;
+        else if (k == "pdl") g_pdl = value != 0;
+        else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -796,6 +966,9 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "subset") *value = ctx->subset;
         else if (k == "fuse_adds") *value = ctx->fuse_adds;
         else if (k == "direct_frames") *value = ctx->direct_frames;
+        else if (k == "dag") *value = ctx->dag;
+        else if (k == "pdl") *value = g_pdl;
+        else if (k == "multicast") *value = ctx->multicast;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
@@ -949,6 +1122,88 @@ int wm_plan_report(const char* variant, int field, uint32_t p, uint64_t m, uint6
         double* base[4] = {nullptr, nullptr, nullptr, nullptr};
         const std::vector<Step> steps = lower(plan, base, dummy);
         fill_report(plan, &steps, report);
+    });
+}
+
+// Diagnostics: dependency DAG of a plan's operations (read / write sets by
+// physical overlap).  out[0] = total cost, out[1] = critical-path cost (cost
+// model: fused frame 9, leaf product 6, block addition 2.5 -- microseconds),
+// out[2] = operations, out[3] = critical path in operations.
+int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, int cutoff,
+                     uint32_t beta, int fuse_frames, double* out) {
+    return guard([&] {
+        Field f;
+        f.p = 65521u;
+        PlanOptions opt;
+        opt.fuse_frames = fuse_frames != 0;
+        Plan plan = plan_variant(variant ? variant : "", f, m, k, n, k, n, n, modp_scalar(f, 1),
+                                 modp_scalar(f, beta), cutoff, opt);
+        const std::size_t N = plan.ops.size();
+        std::vector<std::vector<View>> R(N), Wr(N);
+        std::vector<double> cost(N);
+        for (std::size_t i = 0; i < N; ++i) {
+            const Op& o = plan.ops[i];
+            Wr[i].push_back(o.d);
+            R[i].push_back(o.a);
+            if (o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) R[i].push_back(o.b);
+            if (o.kind == OP_MUL || o.kind == OP_FRAME) R[i].push_back(o.d);
+            if (o.kind == OP_FRAME) {
+                for (const View* h : {&o.h0, &o.h1, &o.h2})
+                    if (h->rows) Wr[i].push_back(*h);
+            }
+            cost[i] = o.kind == OP_FRAME ? 9.0 : o.kind == OP_MUL ? 6.0 : 2.5;
+        }
+        auto hit = [](const std::vector<View>& x, const std::vector<View>& y) {
+            for (const View& a : x)
+                for (const View& b : y)
+                    if (a.phys_overlaps(b)) return true;
+            return false;
+        };
+        std::vector<double> fin(N, 0.0);
+        std::vector<double> depth(N, 0.0);
+        double total = 0, crit = 0, dcrit = 0;
+        for (std::size_t j = 0; j < N; ++j) {
+            double start = 0, d0 = 0;
+            for (std::size_t i = 0; i < j; ++i) {
+                if (fin[i] <= start && depth[i] <= d0) continue;
+                if (hit(Wr[i], R[j]) || hit(Wr[i], Wr[j]) || hit(R[i], Wr[j])) {
+                    start = std::max(start, fin[i]);
+                    d0 = std::max(d0, depth[i]);
+                }
+            }
+            fin[j] = start + cost[j];
+            depth[j] = d0 + 1;
+            total += cost[j];
+            crit = std::max(crit, fin[j]);
+            dcrit = std::max(dcrit, depth[j]);
+        }
+        out[0] = total;
+        out[1] = crit;
+        out[2] = static_cast<double>(N);
+        out[3] = dcrit;
+        // launch level: lanes of the concurrent issue plan
+        wm_ctx dummy;
+        dummy.gemm_engine = 0;
+        dummy.direct_frames = false;
+        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
+        const std::vector<Step> steps = lower(plan, base, dummy);
+        const DagPlan d = plan_dag(steps);
+        int per_lane[kLanes] = {};
+        std::size_t waits = 0;
+        for (std::size_t j = 0; j < steps.size(); ++j) {
+            ++per_lane[d.lane[j]];
+            waits += d.waits[j].size();
+        }
+        out[4] = static_cast<double>(steps.size());
+        for (int l = 0; l < kLanes; ++l) out[5 + l] = per_lane[l];
+        out[5 + kLanes] = static_cast<double>(waits);
+        // kinds of the launches off lane 0: ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
+        for (std::size_t j = 0; j < steps.size(); ++j)
+            if (d.lane[j] != 0) out[10 + steps[j].kind] += 1;
+        if (std::getenv("WM_DAG_DUMP"))
+            for (std::size_t j = 0; j < steps.size() && j < 400; ++j)
+                std::fprintf(stderr, "%zu lane %d kind %d waits %zu\n", j, d.lane[j], steps[j].kind,
+                             d.waits[j].size());
     });
 }
 
@@ -1171,6 +1426,9 @@ int wm_diag_direct_check(wm_ctx* ctx, uint32_t c, int bn, int bconv, uint64_t se
         G.alpha = 1;
         G.pd = static_cast<double>(p);
         G.pinv = 1.0 / G.pd;
+        const bool mcast = bn >= 10000;
+        bn %= 10000;
+        gemm_direct_cluster(G, bn, mcast);
         if (!gemm_direct_supported(G, bn)) fail(E_INVALID, "direct engine: unsupported shape");
         TmaMaps M;
         if (!gemm_direct_encode(G, bn, M)) fail(E_INVALID, "direct engine: tensor map encode failed");

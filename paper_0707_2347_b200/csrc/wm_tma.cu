@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include "wm_launch.h"
 #include "wm_gemm.h"
 #include "wm_tc.h"
 
@@ -420,7 +421,7 @@ cudaError_t launch_cfg(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
     cudaLaunchAttribute attr[2];
     int na = 0;
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    attr[na].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     ++na;
     if (SPLIT > 1) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
