@@ -57,14 +57,44 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle sampler for the timed region (B200_PROFILING.md clocks
+    line).  NVML is polled every millisecond from a thread, so even a few-ms
+    timed region gets samples; nvidia-smi -lms 20 is the fallback."""
+
+    NAMES = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+             ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)]
 
     def __init__(self, index):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reason bits)
+        self.stop = threading.Event()
+        self.thread = None
 
     def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                             mx, int(get_reasons(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.001)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -83,6 +113,9 @@ class Clocks:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -92,7 +125,13 @@ class Clocks:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for (c, m, bits) in self.samples:
+            sm.append(float(c))
+            mx = float(m)
+            for nm, bit in self.NAMES:
+                if bits & bit:
+                    reasons.add(nm)
+        names = [nm for nm, _ in self.NAMES]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
@@ -106,7 +145,8 @@ class Clocks:
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml 1 ms poll" if self.samples else "nvidia-smi -lms 20"}
 
 
 def dist_env():

@@ -144,7 +144,8 @@ struct wm_ctx {
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
     bool dag = true;            // concurrent issue over kLanes streams (dependency DAG)
-    bool multicast = true;      // direct frame GEMM: TMA multicast across N / M tile clusters
+    bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
+                                // SM ingress, not L2 or the issuing TMA unit, bounds the load)
     Lanes lanes;
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
