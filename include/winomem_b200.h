@@ -83,6 +83,11 @@ typedef struct {
      * the whole frames (A, B, beta*C read once, C written once) */
     uint64_t frame_gemm_bytes;
     uint64_t frame_bytes;
+    /* fused frames, per kernel: algorithmic bytes of the prep launches (A, B and
+     * beta*C_in read once, operand planes written once) and of the combine
+     * launches (product planes and packed C_in read once, C written once) */
+    uint64_t frame_prep_bytes;
+    uint64_t frame_comb_bytes;
 } wm_report;
 
 /* ---- library / context --------------------------------------------------- */

@@ -112,7 +112,7 @@ struct CachedPlan {
 
 }  // namespace
 
-constexpr int kLanes = 4;
+constexpr int kLanes = 8;  // maximum; the "dag" option picks how many are used
 
 struct Lanes {
     cudaStream_t s[kLanes] = {};
@@ -143,7 +143,7 @@ struct wm_ctx {
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
-    bool dag = true;            // concurrent issue over kLanes streams (dependency DAG)
+    int dag = 4;                // concurrent issue over this many streams (0/1: one stream)
     bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
                                 // SM ingress, not L2 or the issuing TMA unit, bounds the load)
     Lanes lanes;
@@ -486,6 +486,14 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             op_sets(*op, s.rd, s.wr);
         }
         s.blocks = blk;
+        if (std::getenv("WM_LOWER_DUMP")) {
+            std::fprintf(stderr, "ADD %d:", s.add.n);
+            for (const Op* op : cur)
+                std::fprintf(stderr, " %s/%d(%llux%llu)", op->sched ? op->sched : "-", op->row,
+                             static_cast<unsigned long long>(op->d.rows),
+                             static_cast<unsigned long long>(op->d.cols));
+            std::fprintf(stderr, "\n");
+        }
         steps.push_back(s);
         cur.clear();
     };
@@ -582,9 +590,10 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
 // Concurrent issue.  The memory-lean schedules are mostly a chain, but
 // independent launches exist (about 1.2-1.5x of slack on the configurations'
 // operation DAGs, wm_diag_plan_dag), and every launch here is latency-bound, so
-// running them side by side pays.  Each step goes to one of kLanes streams:
-// the lane of its latest conflicting predecessor (stream order then covers that
-// edge), other conflicting lanes are joined through events.  Dependencies are
+// running them side by side pays.  Each step goes to one of kLanes streams: a
+// lane whose last launch it depends on (stream order then covers that edge and
+// adds no false one), else the lane whose last launch is oldest; conflicting
+// launches on other lanes are joined through events.  Dependencies are
 // exact within an epoch of kEpoch steps; at epoch boundaries every lane joins.
 struct DagPlan {
     std::vector<int> lane;                // per step
@@ -595,7 +604,8 @@ struct DagPlan {
 
 constexpr int kEpoch = 512;
 
-DagPlan plan_dag(const std::vector<Step>& steps) {
+DagPlan plan_dag(const std::vector<Step>& steps, int nl) {
+    nl = nl < 1 ? 1 : nl > kLanes ? kLanes : nl;
     const int n = static_cast<int>(steps.size());
     DagPlan d;
     d.lane.assign(n, 0);
@@ -612,13 +622,13 @@ DagPlan plan_dag(const std::vector<Step>& steps) {
         }
         if (j == epoch0)
             for (int l = 0; l < kLanes; ++l) {
-                last_on[l] = -1;
+                last_on[l] = l < nl ? -1 : 1 << 30;
                 for (int m = 0; m < kLanes; ++m) synced[l][m] = -1;
             }
         // latest conflicting step per lane (earlier ones on a lane are implied)
         int dep[kLanes];
         for (int l = 0; l < kLanes; ++l) dep[l] = -1;
-        int open = kLanes;
+        int open = nl;
         for (int i = j - 1; i >= epoch0 && open > 0; --i) {
             const int l = d.lane[i];
             if (dep[l] >= 0) continue;
@@ -627,13 +637,15 @@ DagPlan plan_dag(const std::vector<Step>& steps) {
                 --open;
             }
         }
+        // a lane whose last launch is itself a dependency adds no false edge;
+        // otherwise take the lane whose last launch is oldest (most likely done)
         int best = -1;
-        for (int l = 0; l < kLanes; ++l)
-            if (dep[l] >= 0 && (best < 0 || dep[l] > dep[best])) best = l;
+        for (int l = 0; l < nl; ++l)
+            if (last_on[l] >= 0 && dep[l] == last_on[l] && (best < 0 || last_on[l] > last_on[best]))
+                best = l;
         if (best < 0) {
-            // independent of the epoch so far: the least recently used lane
             best = 0;
-            for (int l = 1; l < kLanes; ++l)
+            for (int l = 1; l < nl; ++l)
                 if (last_on[l] < last_on[best]) best = l;
         }
         d.lane[j] = best;
@@ -649,12 +661,13 @@ DagPlan plan_dag(const std::vector<Step>& steps) {
 }
 
 void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cudaStream_t main,
-               Lanes& L) {
+               Lanes& L, int nl) {
+    nl = nl < 1 ? 1 : nl > kLanes ? kLanes : nl;
     const int n = static_cast<int>(steps.size());
     L.s[0] = main;
-    for (int l = 1; l < kLanes; ++l)
+    for (int l = 1; l < nl; ++l)
         if (!L.s[l]) WM_CUDA(cudaStreamCreateWithFlags(&L.s[l], cudaStreamNonBlocking));
-    for (int l = 0; l < kLanes; ++l)
+    for (int l = 0; l < nl; ++l)
         if (!L.join[l]) WM_CUDA(cudaEventCreateWithFlags(&L.join[l], cudaEventDisableTiming));
     while (static_cast<int>(L.ev.size()) < n) {
         cudaEvent_t e;
@@ -663,10 +676,10 @@ void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cuda
     }
     auto fork = [&]() {  // every lane starts after what is already on the main stream
         WM_CUDA(cudaEventRecord(L.join[0], main));
-        for (int l = 1; l < kLanes; ++l) WM_CUDA(cudaStreamWaitEvent(L.s[l], L.join[0], 0));
+        for (int l = 1; l < nl; ++l) WM_CUDA(cudaStreamWaitEvent(L.s[l], L.join[0], 0));
     };
     auto join = [&]() {  // the main stream continues after every lane
-        for (int l = 1; l < kLanes; ++l) {
+        for (int l = 1; l < nl; ++l) {
             WM_CUDA(cudaEventRecord(L.join[l], L.s[l]));
             WM_CUDA(cudaStreamWaitEvent(main, L.join[l], 0));
         }
@@ -721,6 +734,14 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
             if (s.kind == Step::FPREP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fprep.c) * s.fprep.c;
                 r->frame_bytes += (4 + 4 + 4 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double);
+                int planes = 0;
+                for (int i = 0; i < PL_COUNT; ++i) planes += s.fprep.plane[i] != nullptr;
+                r->frame_prep_bytes += (8 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double) +
+                                       planes * c2 * 2 + (s.fprep.beta ? c2 * 8 : 0);
+            }
+            if (s.kind == Step::FCOMB) {
+                const std::uint64_t c2 = static_cast<std::uint64_t>(s.fcomb.c) * s.fcomb.c;
+                r->frame_comb_bytes += 7 * c2 * 2 + (s.fcomb.beta ? c2 * 8 : 0) + 4 * c2 * sizeof(double);
             }
             if (s.kind == Step::GROUP) {
                 const fused::GroupDesc& G = fused::kGroups[s.gid];
@@ -791,10 +812,10 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
         cp = ctx->cache.front().second.get();
     }
-    const bool dag = ctx->dag && ctx->subset == 0 && cp->steps.size() > 1;
-    if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps));
+    const bool dag = ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1;
+    if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps, ctx->dag));
     auto go = [&]() {
-        if (dag) issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes);
+        if (dag) issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes, ctx->dag);
         else issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
     };
     if (ctx->graphs && cp->steps.size() > 1) {
@@ -947,7 +968,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "subset") ctx->subset = static_cast<int>(value);
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
         else if (k == "direct_frames") ctx->direct_frames = value != 0;
-        else if (k == "dag") ctx->dag = value != 0;
+        else if (k == "dag") ctx->dag = static_cast<int>(value);
         else if (k == "pdl") g_pdl = value != 0;
         else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
@@ -1188,16 +1209,16 @@ int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, in
         dummy.direct_frames = false;
         double* base[4] = {nullptr, nullptr, nullptr, nullptr};
         const std::vector<Step> steps = lower(plan, base, dummy);
-        const DagPlan d = plan_dag(steps);
-        int per_lane[kLanes] = {};
+        const DagPlan d = plan_dag(steps, 4);
+        int per_lane[kLanes] = {};  // (4 lanes)
         std::size_t waits = 0;
         for (std::size_t j = 0; j < steps.size(); ++j) {
             ++per_lane[d.lane[j]];
             waits += d.waits[j].size();
         }
         out[4] = static_cast<double>(steps.size());
-        for (int l = 0; l < kLanes; ++l) out[5 + l] = per_lane[l];
-        out[5 + kLanes] = static_cast<double>(waits);
+        for (int l = 0; l < 4; ++l) out[5 + l] = per_lane[l];
+        out[9] = static_cast<double>(waits);
         // kinds of the launches off lane 0: ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
         for (std::size_t j = 0; j < steps.size(); ++j)
             if (d.lane[j] != 0) out[10 + steps[j].kind] += 1;

@@ -160,6 +160,8 @@ class CostReport:
     add_bytes_issued: int = 0
     frame_gemm_bytes: int = 0
     frame_bytes: int = 0
+    frame_prep_bytes: int = 0
+    frame_comb_bytes: int = 0
 
     def ops(self):
         return self.mults + self.adds
@@ -184,7 +186,8 @@ def _report(variant, m, k, n, cutoff, r: wm_report) -> CostReport:
     return CostReport(variant, m, k, n, cutoff, r.mults, r.adds, r.peak_extra_words,
                       r.total_alloc_words, r.word_moves, r.classical_calls, calls,
                       r.peak_extra_bytes, r.n_ops, r.n_launches, r.fused_frames, r.add_bytes,
-                      r.leaf_flops, r.add_bytes_issued, r.frame_gemm_bytes, r.frame_bytes)
+                      r.leaf_flops, r.add_bytes_issued, r.frame_gemm_bytes, r.frame_bytes,
+                      r.frame_prep_bytes, r.frame_comb_bytes)
 
 
 # ---- device context ------------------------------------------------------
