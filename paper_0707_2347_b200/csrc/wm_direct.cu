@@ -39,7 +39,7 @@
 namespace wm {
 namespace {
 
-constexpr int BM = 128, KT = 128, NS = 4;
+constexpr int BM = 128, KT = 128;
 // A tiles are K-major with a KT-byte swizzle span (SW64 for KT = 64)
 constexpr std::uint64_t A_LAYOUT = KT == 128 ? 2 : 4;  // UMMA SWIZZLE_128B / SWIZZLE_64B
 constexpr int NEPI = 256;           // eight epilogue / B-loader warps
@@ -50,15 +50,16 @@ template <int BN>
 struct DCfg {
     static constexpr int B_PART = KT * BN;
     static constexpr int STAGE = 2 * A_PART + 2 * B_PART;  // 20 KB (BN 32) / 24 KB (BN 64)
-    static constexpr std::uint32_t TCOLS = BN == 32 ? 128 : 256;
+    static constexpr std::uint32_t TCOLS = BN == 32 ? 128 : BN == 64 ? 256 : 512;  // 4 BN columns
+    static constexpr int NS = BN == 128 ? 3 : 4;  // stage ring depth (<= ~200 KB)
     // UMMA layout type of the MN-major B tile (swizzle span = BN bytes)
-    static constexpr std::uint64_t B_LAYOUT = BN == 32 ? 6 : 4;  // SWIZZLE_32B / SWIZZLE_64B
+    static constexpr std::uint64_t B_LAYOUT = BN == 32 ? 6 : BN == 64 ? 4 : 2;  // SW32 / SW64 / SW128
 };
 
 template <int BN>
 struct DSmem {
-    std::uint8_t stage[NS][DCfg<BN>::STAGE];  // 1024-B aligned
-    std::uint64_t full[NS], empty[NS];
+    std::uint8_t stage[DCfg<BN>::NS][DCfg<BN>::STAGE];  // 1024-B aligned
+    std::uint64_t full[DCfg<BN>::NS], empty[DCfg<BN>::NS];
     std::uint64_t done;
     std::uint32_t tmem_base;
 };
@@ -122,8 +123,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 // byte offset of B element (k, n) in a BN-byte-swizzled MN-major limb tile
 template <int BN>
 __device__ __forceinline__ std::uint32_t boff(std::uint32_t k, std::uint32_t n) {
-    constexpr std::uint32_t mask = BN == 32 ? 1u : 3u;
-    constexpr std::uint32_t sh = BN == 32 ? 2u : 1u;
+    constexpr std::uint32_t mask = BN == 32 ? 1u : BN == 64 ? 3u : 7u;
+    constexpr std::uint32_t sh = BN == 32 ? 2u : BN == 64 ? 1u : 0u;
     return k * BN + ((((n >> 4) ^ (k >> sh)) & mask) << 4) + (n & 15u);
 }
 
@@ -190,6 +191,7 @@ template <int BN, int BSRC>
 __global__ void __launch_bounds__(NT, 1)
     k_gemm_direct(const __grid_constant__ GemmParams P, const __grid_constant__ TmaMaps M) {
     using C = DCfg<BN>;
+    constexpr int NS = C::NS;
     extern __shared__ std::uint8_t smem_raw[];
     const std::uint32_t base = tc::smem_u32(smem_raw);
     DSmem<BN>& S = *reinterpret_cast<DSmem<BN>*>(smem_raw + ((1024 - (base & 1023)) & 1023));
@@ -371,6 +373,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 template <int BN>
 constexpr std::size_t dsmem_bytes() {
+    static_assert(sizeof(DSmem<BN>) + 1024 <= 232448, "shared memory budget");
     return sizeof(DSmem<BN>) + 1024;
 }
 
@@ -434,6 +437,7 @@ cudaError_t gemm_direct_init() {
     cudaError_t e;
     if ((e = dset_attr<32, 0>()) != cudaSuccess) return e;
     if ((e = dset_attr<64, 0>()) != cudaSuccess) return e;
+    if ((e = dset_attr<128, 0>()) != cudaSuccess) return e;
     if ((e = dset_attr<32, 1>()) != cudaSuccess) return e;
     if ((e = dset_attr<64, 1>()) != cudaSuccess) return e;
     g_direct_ok = true;
@@ -441,8 +445,9 @@ cudaError_t gemm_direct_init() {
 }
 
 bool gemm_direct_supported(const GemmParams& P, int bn) {
+    const bool lsu = bn >= 1000;
     bn %= 1000;
-    if (!g_direct_ok || (bn != 32 && bn != 64)) return false;
+    if (!g_direct_ok || (bn != 32 && bn != 64 && bn != 128) || (lsu && bn == 128)) return false;
     if (P.m % BM || P.n % bn || P.k % KT || P.k > 32768 || P.nprod < 1 || P.nprod > kMaxProducts)
         return false;
     for (std::uint32_t i = 0; i < P.nprod; ++i) {
@@ -456,7 +461,9 @@ bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
     bn %= 1000;
     if (!g_denc) return false;
     std::memset(&M, 0, sizeof(M));
-    const CUtensorMapSwizzle bsw = bn == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B;
+    const CUtensorMapSwizzle bsw = bn == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                   : bn == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                              : CU_TENSOR_MAP_SWIZZLE_128B;
     const bool mc = P.mc_n * P.mc_m > 1;
     const std::uint32_t mn = mc ? P.mc_n : 1, mm = mc ? P.mc_m : 1, bl = mc ? 1 : 2;
     for (std::uint32_t i = 0; i < P.nprod; ++i) {
@@ -470,10 +477,18 @@ bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
     return true;
 }
 
-// (BN) for a direct product set: BN 32 unless that leaves the SMs oversubscribed
+// BN for a direct product set: the narrowest tile that still fits the grid in
+// one wave of the 148 SMs (every CTA must receive its whole 128 x K A panel, so
+// fewer, wider tiles win once the grid would need a second wave)
 int gemm_direct_choose(const GemmParams& P) {
-    const std::uint32_t ctas32 = P.tiles_m * P.nprod * (P.n / 32);
-    return (ctas32 > 2 * 148 && P.n % 64 == 0) ? 64 : 32;
+    const std::uint32_t mt = P.tiles_m * P.nprod;
+    // a float64 B is streamed at 8 B / element: keep its panels narrow
+    bool bconv = false;
+    for (std::uint32_t i = 0; i < P.nprod; ++i) bconv |= P.b[i].fmt == 0;
+    const int widest = bconv ? 64 : 128;
+    for (int bn : {32, 64, 128})
+        if (bn <= widest && P.n % bn == 0 && mt * (P.n / bn) <= 148) return bn;
+    return P.n % widest == 0 ? widest : P.n % 64 == 0 ? 64 : 32;
 }
 
 // Multicast cluster for a direct launch (sets P.mc_n / P.mc_m): up to 4 N tiles
@@ -481,7 +496,8 @@ int gemm_direct_choose(const GemmParams& P) {
 void gemm_direct_cluster(GemmParams& P, int bn, bool enable) {
     bn %= 1000;
     P.mc_n = P.mc_m = 1;
-    if (!enable || P.k / KT > static_cast<std::uint32_t>(NS)) return;
+    const int ns = bn == 128 ? DCfg<128>::NS : DCfg<32>::NS;
+    if (!enable || bn == 128 || P.k / KT > static_cast<std::uint32_t>(ns)) return;
     const std::uint32_t nt = P.n / bn;
     P.mc_n = nt % 4 == 0 ? 4 : nt % 2 == 0 ? 2 : 1;
     P.mc_m = P.tiles_m % 2 == 0 ? 2 : 1;
@@ -492,6 +508,7 @@ cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cu
     switch (bn) {
         case 32: return dlaunch<32, 0>(P, M, s);
         case 64: return dlaunch<64, 0>(P, M, s);
+        case 128: return dlaunch<128, 0>(P, M, s);
         case 1032: return dlaunch<32, 1>(P, M, s);
         case 1064: return dlaunch<64, 1>(P, M, s);
         default: return cudaErrorInvalidValue;

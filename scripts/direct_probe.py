@@ -18,7 +18,7 @@ L.wm_diag_direct_check.restype = C.c_int
 ctx = W.Context(p=65521)
 res = {}
 for c in (128, 256, 512):
-    for bn in (32, 64):
+    for bn in (32, 64, 128):
         for bconv in (0, 1):
             bad = C.c_uint64()
             us = C.c_double()

@@ -165,7 +165,7 @@ def test_config_full_size_hash(W, name, fused):
 
 
 @pytest.mark.parametrize("c", [128, 256, 512])
-@pytest.mark.parametrize("bn", [32, 64, 1032])
+@pytest.mark.parametrize("bn", [32, 64, 128, 1032])
 @pytest.mark.parametrize("bconv", [0, 1], ids=["planes", "f64-B"])
 def test_direct_limb_gemm(W, c, bn, bconv):
     """Seven-product direct-limb frame GEMM on random limb planes (one product
