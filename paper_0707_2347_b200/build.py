@@ -25,6 +25,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", CSRC, "-I", INC,
           "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+# measurement builds only (e.g. WM_NVCC_FLAGS=-DWM_EPI_MODE=1); never set for the product
+COMMON += os.environ.get("WM_NVCC_FLAGS", "").split()
 
 
 def _sources():
