@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1)
     const std::uint32_t tbase = S.tmem_base;
     if (tid == 32) WM_DSTAMP(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_C();
     if (tid == 32) WM_DSTAMP(2);
 
     if (warp == 0) {
@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
     }
 
+    WM_PDL_LATE_C();
     const double p = P.pd, pinv = P.pinv;
     if (warp >= 2) {
         tc::mbar_wait(&S.done, 0);

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(128) k_leaf_dmma(const MulParams P) {
     const std::uint64_t col0 = static_cast<std::uint64_t>(blockIdx.x) * BN;
     const std::uint32_t M = P.m, N = P.n, K = P.k;
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_C();
 
     auto load_tile = [&](int buf, std::uint32_t k0) {
 #pragma unroll
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(128) k_leaf_dmma(const MulParams P) {
         }
         __syncthreads();
     }
+    WM_PDL_LATE_C();
 
     const double p = P.pd, pinv = P.pinv;
     const double al = REAL ? P.alphad : static_cast<double>(P.alpha);

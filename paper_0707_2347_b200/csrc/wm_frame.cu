@@ -63,7 +63,7 @@ __device__ __forceinline__ uint2 pack(double a, double b, double c, double d) {
 // beta*C_in) before a barrier, then write their halves of the slots.
 __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_M();
     const std::uint32_t c4 = P.c / 4;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     const bool live = idx < static_cast<std::uint64_t>(P.c) * c4 * 2;
@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
             *reinterpret_cast<std::uint32_t*>(c11 + 4 * (r * P.C.ld + q + k * c4) + 2 * h) =
                 static_cast<std::uint32_t>(cin[k][0]) | (static_cast<std::uint32_t>(cin[k][1]) << 16);
     }
+    WM_PDL_LATE_M();
 }
 
 // Limb-pair variant for the direct-limb GEMM (wm_direct.cu): one CTA per row r,
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
 // CTA's barrier, so the in-place packing stays race-free.
 __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_M();
     const std::uint64_t r = blockIdx.x, j = 2 * threadIdx.x;
     const double p = P.pd, pinv = P.pinv;
     double a11[2], a12[2], a21[2], a22[2], b11[2], b12[2], b21[2], b22[2];
@@ -217,12 +218,13 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
                 static_cast<std::uint32_t>(cin[0][e]) | (static_cast<std::uint32_t>(cin[1][e]) << 16),
                 static_cast<std::uint32_t>(cin[2][e]) | (static_cast<std::uint32_t>(cin[3][e]) << 16));
     }
+    WM_PDL_LATE_M();
 }
 
 // thread (r, 2 consecutive columns j, j+1) of the quadrant
 __global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_M();
     const std::uint32_t c2 = P.c / 2;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     if (idx >= static_cast<std::uint64_t>(P.c) * c2) return;
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
 #pragma unroll
     for (int qd = 0; qd < 4; ++qd)
         *reinterpret_cast<double2*>(P.C.q[qd] + r * P.C.ld + j) = make_double2(out[qd][0], out[qd][1]);
+    WM_PDL_LATE_M();
 }
 
 template <class K, class Prm>

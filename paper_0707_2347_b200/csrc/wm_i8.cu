@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_i8(const GemmParams P) {
     tc::fence_after();
     const std::uint32_t tbase = S.tmem_base;
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_C();
 
     // 16-B units per chunk: A rows of KC residues, B rows of BN residues
     const int a_upr = a16 ? KC / 8 : KC / 2;   // units per A row
@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(NT, 1) k_gemm_i8(const GemmParams P) {
     }
 
     // ---------------- epilogue (converter warps): TMEM -> exact recombination
+    WM_PDL_LATE_C();
     const double p = P.pd, pinv = P.pinv;
     const double al = static_cast<double>(P.alpha), be = static_cast<double>(P.beta);
     tc::mbar_wait(&S.done, 0);

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
     // programmatic dependent launch: wait for the producer grid, then let the
     // next kernel in the chain start its launch
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_M();
     int i = 0;
 #pragma unroll 1
     while (i + 1 < B.n && blockIdx.x >= B.it[i + 1].blk0) ++i;
@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
             t.d[rr * t.ldd + cc] = apply<REAL>(a, b, mode, sa, sb, p, pinv);
         }
     }
+    WM_PDL_LATE_M();
 }
 
 }  // namespace
@@ -127,13 +128,14 @@ namespace {
 template <bool REAL>
 __global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams G) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_M();
     const std::uint32_t cv = G.cols >> 1;
     const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * cv;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     if (idx >= total) return;
     const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
     fused::group_dispatch<REAL>(gid, G, r, c);
+    WM_PDL_LATE_M();
 }
 
 __global__ void k_u32_to_f64(double* __restrict__ dst, std::uint64_t ldd,

@@ -6,3 +6,30 @@ namespace wm {
 // option turns it off for measurements).
 extern bool g_pdl;
 }  // namespace wm
+
+// Where a kernel lets its programmatic dependents launch.  A dependent launched
+// early parks its CTAs at griddepcontrol.wait on the SMs the running kernel
+// uses; for compute-bound kernels that costs issue slots (measured: the float64
+// DMMA leaf chain of config 5 ran 1.8x slower), so those trigger after their
+// main loop.  0 = right after griddepcontrol.wait, 1 = late.
+#ifndef WM_PDL_LATE_COMPUTE
+#define WM_PDL_LATE_COMPUTE 1
+#endif
+#ifndef WM_PDL_LATE_MEMORY
+#define WM_PDL_LATE_MEMORY 0
+#endif
+#define WM_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory")
+#if WM_PDL_LATE_COMPUTE
+#define WM_PDL_EARLY_C()
+#define WM_PDL_LATE_C() WM_PDL_TRIGGER()
+#else
+#define WM_PDL_EARLY_C() WM_PDL_TRIGGER()
+#define WM_PDL_LATE_C()
+#endif
+#if WM_PDL_LATE_MEMORY
+#define WM_PDL_EARLY_M()
+#define WM_PDL_LATE_M() WM_PDL_TRIGGER()
+#else
+#define WM_PDL_EARLY_M() WM_PDL_TRIGGER()
+#define WM_PDL_LATE_M()
+#endif

@@ -551,7 +551,41 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
     return steps;
 }
 
-void issue_one(const Step& s, bool real, cudaStream_t st) {
+// A launch long enough (tens of microseconds) that its successor gains nothing
+// from launching early.
+bool long_step(const Step& s) {
+    switch (s.kind) {
+        case Step::ADD: {
+            std::uint64_t e = 0;
+            for (int i = 0; i < s.add.n; ++i) e += static_cast<std::uint64_t>(s.add.it[i].rows) * s.add.it[i].cols;
+            return e > (4ull << 20);
+        }
+        case Step::GROUP: return static_cast<std::uint64_t>(s.grp.rows) * s.grp.cols > (4ull << 20);
+        case Step::MUL:
+            return 2.0 * s.mul.m * static_cast<double>(s.mul.k) * s.mul.n > 1e9;
+        case Step::FPREP: return s.fprep.c >= 1024;
+        case Step::FGEMM: return s.fgemm.m >= 1024;
+        case Step::FCOMB: return s.fcomb.c >= 1024;
+        default: return false;
+    }
+}
+
+bool g_pdl_user = true;  // the "pdl" option; per launch g_pdl = option && policy below
+
+// Programmatic dependent launch per launch: not after a long predecessor (no
+// latency left to hide), and never for a multi-CTA-per-SM compute kernel: its
+// CTAs would be placed while the predecessor still fills the SMs, bunch up on
+// the few SMs with room and keep that placement (measured: config 5's 1024^3
+// float64 leaves, 2.88 s per multiply with PDL vs 1.68 s without).
+bool use_pdl(const Step& s, const Step* prev) {
+    if (!g_pdl_user || (prev && long_step(*prev))) return false;
+    if (s.kind == Step::MUL && 2.0 * s.mul.m * static_cast<double>(s.mul.k) * s.mul.n > 1e8)
+        return false;
+    return true;
+}
+
+void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nullptr) {
+    g_pdl = use_pdl(s, prev);
     switch (s.kind) {
         case Step::ADD: WM_CUDA(launch_addsub(s.add, real, s.blocks, st)); break;
         case Step::MUL:
@@ -575,6 +609,7 @@ void issue_one(const Step& s, bool real, cudaStream_t st) {
 }
 
 void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subset = 0) {
+    const Step* prev = nullptr;
     for (const Step& s : steps) {
         if (subset == 1 && s.kind != Step::ADD && s.kind != Step::GROUP) continue;
         if (subset == 2 && s.kind != Step::MUL) continue;
@@ -583,7 +618,8 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
         if (subset == 4 && s.kind != Step::FPREP) continue;
         if (subset == 5 && s.kind != Step::FGEMM) continue;
         if (subset == 6 && s.kind != Step::FCOMB) continue;
-        issue_one(s, real, st);
+        issue_one(s, real, st, prev);
+        prev = &s;
     }
 }
 
@@ -685,10 +721,13 @@ void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cuda
         }
     };
     fork();
+    int last[kLanes];
+    for (int l = 0; l < kLanes; ++l) last[l] = -1;
     for (int j = 0; j < n; ++j) {
         cudaStream_t st = L.s[d.lane[j]];
         for (int i : d.waits[j]) WM_CUDA(cudaStreamWaitEvent(st, L.ev[i], 0));
-        issue_one(steps[j], real, st);
+        issue_one(steps[j], real, st, last[d.lane[j]] >= 0 ? &steps[last[d.lane[j]]] : nullptr);
+        last[d.lane[j]] = j;
         if (d.record[j]) WM_CUDA(cudaEventRecord(L.ev[j], st));
         if (d.epoch_end[j]) {
             join();
@@ -969,7 +1008,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "fuse_adds") ctx->fuse_adds = value != 0;
         else if (k == "direct_frames") ctx->direct_frames = value != 0;
         else if (k == "dag") ctx->dag = static_cast<int>(value);
-        else if (k == "pdl") g_pdl = value != 0;
+        else if (k == "pdl") g_pdl_user = value != 0;
         else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -989,7 +1028,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "fuse_adds") *value = ctx->fuse_adds;
         else if (k == "direct_frames") *value = ctx->direct_frames;
         else if (k == "dag") *value = ctx->dag;
-        else if (k == "pdl") *value = g_pdl;
+        else if (k == "pdl") *value = g_pdl_user;
         else if (k == "multicast") *value = ctx->multicast;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;

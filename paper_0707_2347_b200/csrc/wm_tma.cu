@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(NT, 1)
     const std::uint32_t tbase = S.tmem_base;
     if (tid == 64) WM_STAMP(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    WM_PDL_EARLY_C();
     if (tid == 64) WM_STAMP(2);
 
     if (warp == 0) {
@@ -278,6 +278,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
     }
 
+    WM_PDL_LATE_C();
     const double p = P.pd, pinv = P.pinv;
     const double al = static_cast<double>(P.alpha), be = static_cast<double>(P.beta);
     if (tid == 64) WM_STAMP(4);
