@@ -88,6 +88,8 @@ typedef struct {
      * launches (product planes and packed C_in read once, C written once) */
     uint64_t frame_prep_bytes;
     uint64_t frame_comb_bytes;
+    /* classical leaf flops (2*m*k*n) executed inside fused frames */
+    uint64_t frame_leaf_flops;
 } wm_report;
 
 /* ---- library / context --------------------------------------------------- */

@@ -765,6 +765,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                 const std::uint64_t mk = static_cast<std::uint64_t>(G.m) * G.k,
                                     kn = static_cast<std::uint64_t>(G.k) * G.n,
                                     mn = static_cast<std::uint64_t>(G.m) * G.n;
+                r->frame_leaf_flops += 2ull * G.m * G.k * G.n * G.nprod;
                 for (std::uint32_t i = 0; i < G.nprod; ++i)
                     r->frame_gemm_bytes += mk * (G.a[i].fmt != 0 ? 2 : 8) +
                                            kn * (G.b[i].fmt != 0 ? 2 : 8) +
