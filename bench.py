@@ -8,9 +8,10 @@ SplitMix64 seeds A=2, B=3, C=4 stored as float64, cutoff 256 (depth 4).
 A step is one full multiplication with the inputs resident in HBM; the
 400 MB of inputs exceed the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the same
-single-GPU workload on its own device (replicas, weak scaling); ranks are timed
-on the device and the max over ranks is reported.
+Multi-GPU (torchrun, one process per GPU): the 7 top-level Winograd products of
+ONE multiplication are partitioned over the ranks (paper_0707_2347_b200/dist.py;
+NCCL point-to-point carries operand blocks out and products back), strong
+scaling; ranks are timed on the device and the max over ranks is reported.
 
 ``--impl reference`` times the reference's own CPU implementation (the
 unmodified winomem headers compiled into oracle/_ref) on the host cores.
@@ -431,11 +432,16 @@ def main():
     dominant = max(single, key=lambda k_: rooflines[k_]["seconds_per_step"] or 0.0)
     dom = rooflines[dominant]
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "r1", "traffic_%s.json" % args.config.lower())
-    if os.path.exists(tfile):  # dram bytes per launch from a committed ncu --set full capture
-        traffic = json.load(open(tfile)).get(dominant)
+    # dram read + write bytes of the class per step, summed over its launches in the
+    # committed ncu launch list (scripts/ncu_launch_summary.py; ncu replays each
+    # launch serialised with a cold cache)
+    tfile = os.path.join(ROOT, "profiles", "r1", "ncu_launch_summary_%s.json" % args.config.lower())
+    if os.path.exists(tfile):
+        cls = json.load(open(tfile)).get("classes", {}).get(dominant)
+        traffic = cls.get("dram_bytes_per_step") if cls else None
     roof = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
             "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
+            "traffic_unit": "dram bytes per step (class total, ncu capture)",
             "peak_source": dom.get("peak_source") or hbm_src, "class": dominant,
             "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
             "kernel_seconds_per_step": dom["seconds_per_step"]}
@@ -564,11 +570,18 @@ def run_partitioned(args, cfg, rank, world, local):
 def e2e(W, cfg, args, np, torch):
     """Same metric through the public host API: pinned u32 host buffers in,
     result out, host<->device copies inside the timed region."""
-    from oracle import oracle as O  # inputs only (seeded generator), not timed
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
-    A = torch.from_numpy(O.fill_random(m, k, cfg["seed"])).pin_memory().numpy()
-    B = torch.from_numpy(O.fill_random(k, n, cfg["seed"] + 1)).pin_memory().numpy()
-    C0 = O.fill_random(m, n, cfg["seed"] + 2) if cfg["beta"] else np.zeros((m, n), np.uint32)
+
+    def host_input(rows, cols, seed):  # the package's own SplitMix64 fill, downloaded once (untimed)
+        M = W.Matrix(rows, cols)
+        M.fill_random(seed)
+        out = M.to_u32()
+        del M
+        return out
+
+    A = torch.from_numpy(host_input(m, k, cfg["seed"])).pin_memory().numpy()
+    B = torch.from_numpy(host_input(k, n, cfg["seed"] + 1)).pin_memory().numpy()
+    C0 = host_input(m, n, cfg["seed"] + 2) if cfg["beta"] else np.zeros((m, n), np.uint32)
     Cp = torch.from_numpy(C0.copy()).pin_memory().numpy()
     ctx = W.Context.get()
     ctx.set_option("leaf_kernel", args.leaf)

@@ -57,6 +57,40 @@ __device__ __forceinline__ uint2 pack(double a, double b, double c, double d) {
                       static_cast<std::uint32_t>(c) | (static_cast<std::uint32_t>(d) << 16));
 }
 
+// The four quadrant values (row r, columns j, j+1) of a frame operand: loaded
+// from its view, or -- folded -- computed from the sources of the parent
+// addition(s) that produce it (sa*s0 + sb*s1 < 2^33: exact, one reduction).
+__device__ __forceinline__ void load_operand(const FrameQuads& X, const FrameFold& F,
+                                             std::uint64_t r, std::uint64_t j, double p,
+                                             double pinv, double (&v)[4][2]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!F.on) {
+            const double2 x = *reinterpret_cast<const double2*>(X.q[k] + r * X.ld + j);
+            v[k][0] = x.x;
+            v[k][1] = x.y;
+            continue;
+        }
+        const double2 a = *reinterpret_cast<const double2*>(F.s0[k] + r * F.ld0 + j);
+        double2 b = make_double2(0.0, 0.0);
+        if (F.s1[0]) b = *reinterpret_cast<const double2*>(F.s1[k] + r * F.ld1 + j);
+        v[k][0] = rmod(fma(F.sa, a.x, F.sb * b.x), p, pinv);
+        v[k][1] = rmod(fma(F.sa, a.y, F.sb * b.y), p, pinv);
+    }
+}
+
+// Store a folded operand into its own view when a later operation reads it.
+// Every position is written by the thread that read it (the sources are either
+// this view itself, same window, or disjoint from it).
+__device__ __forceinline__ void store_operand(const FrameQuads& X, const FrameFold& F,
+                                              std::uint64_t r, std::uint64_t j,
+                                              const double (&v)[4][2]) {
+    if (!F.on || !F.writeback) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        *reinterpret_cast<double2*>(X.q[k] + r * X.ld + j) = make_double2(v[k][0], v[k][1]);
+}
+
 // thread (r, q, h), q < c/4, h in {0,1}: plane columns j = 4q + 2h, +1; the
 // float64 slots (r, q + k c/4), k = 0..3, of every host / C block are owned by
 // the thread pair (q, 0), (q, 1) of one CTA: both read all they need (A, B and
@@ -72,22 +106,13 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     const std::uint64_t j = 4 * q + 2 * h;
     const double p = P.pd, pinv = P.pinv;
 
-    double a11[2], a12[2], a21[2], a22[2], b11[2], b12[2], b21[2], b22[2];
-    auto ld2 = [&](const double* ptr, double (&v)[2]) {
-        const double2 x = *reinterpret_cast<const double2*>(ptr);
-        v[0] = x.x;
-        v[1] = x.y;
-    };
+    double av[4][2], bv[4][2];
+    double(&a11)[2] = av[0], (&a12)[2] = av[1], (&a21)[2] = av[2], (&a22)[2] = av[3];
+    double(&b11)[2] = bv[0], (&b12)[2] = bv[1], (&b21)[2] = bv[2], (&b22)[2] = bv[3];
     double cin[4][2];  // [k][quadrant 2h, 2h+1]
     if (live) {
-        ld2(P.A.q[0] + r * P.A.ld + j, a11);
-        ld2(P.A.q[1] + r * P.A.ld + j, a12);
-        ld2(P.A.q[2] + r * P.A.ld + j, a21);
-        ld2(P.A.q[3] + r * P.A.ld + j, a22);
-        ld2(P.B.q[0] + r * P.B.ld + j, b11);
-        ld2(P.B.q[1] + r * P.B.ld + j, b12);
-        ld2(P.B.q[2] + r * P.B.ld + j, b21);
-        ld2(P.B.q[3] + r * P.B.ld + j, b22);
+        load_operand(P.A, P.fold[0], r, j, p, pinv, av);
+        load_operand(P.B, P.fold[1], r, j, p, pinv, bv);
         if (P.beta != 0) {
             const double be = static_cast<double>(P.beta);
 #pragma unroll
@@ -99,6 +124,8 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     }
     __syncthreads();  // every owned slot has been read before any is overwritten
     if (!live) return;
+    store_operand(P.A, P.fold[0], r, j, av);
+    store_operand(P.B, P.fold[1], r, j, bv);
     double s[4][2], t[4][2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -150,20 +177,16 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
     WM_PDL_EARLY_M();
     const std::uint64_t r = blockIdx.x, j = 2 * threadIdx.x;
     const double p = P.pd, pinv = P.pinv;
-    double a11[2], a12[2], a21[2], a22[2], b11[2], b12[2], b21[2], b22[2];
+    double av[4][2], bv[4][2];
+    double(&a11)[2] = av[0], (&a12)[2] = av[1], (&a21)[2] = av[2], (&a22)[2] = av[3];
+    double(&b11)[2] = bv[0], (&b12)[2] = bv[1], (&b21)[2] = bv[2], (&b22)[2] = bv[3];
+    load_operand(P.A, P.fold[0], r, j, p, pinv, av);
+    load_operand(P.B, P.fold[1], r, j, p, pinv, bv);
     auto ld2 = [&](const double* ptr, double (&v)[2]) {
         const double2 x = *reinterpret_cast<const double2*>(ptr);
         v[0] = x.x;
         v[1] = x.y;
     };
-    ld2(P.A.q[0] + r * P.A.ld + j, a11);
-    ld2(P.A.q[1] + r * P.A.ld + j, a12);
-    ld2(P.A.q[2] + r * P.A.ld + j, a21);
-    ld2(P.A.q[3] + r * P.A.ld + j, a22);
-    ld2(P.B.q[0] + r * P.B.ld + j, b11);
-    ld2(P.B.q[1] + r * P.B.ld + j, b12);
-    ld2(P.B.q[2] + r * P.B.ld + j, b21);
-    ld2(P.B.q[3] + r * P.B.ld + j, b22);
     double cin[4][2];  // [quadrant][column]
     if (P.beta != 0) {
         const double be = static_cast<double>(P.beta);
@@ -176,6 +199,8 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
         }
     }
     __syncthreads();  // row r of every host has been read before any of it is overwritten
+    store_operand(P.A, P.fold[0], r, j, av);
+    store_operand(P.B, P.fold[1], r, j, bv);
     double s[4][2], t[4][2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {

@@ -17,8 +17,21 @@ struct FrameQuads {
 enum FramePlane { PL_S1, PL_S2, PL_S3, PL_S4, PL_T1, PL_T2, PL_T3, PL_T4,
                   PL_A11, PL_A12, PL_A22, PL_B11, PL_B21, PL_B22, PL_COUNT };
 
+// A frame operand folded from the parent schedule's addition(s) that produce it
+// (lowering pass, wm_runtime.cu): operand = sa*s0 + sb*s1 mod p, computed by the
+// prep from the sources; `writeback` also stores it into the operand's own view
+// when a later operation still reads it.
+struct FrameFold {
+    const double* s0[4];   // quadrants of the first source
+    const double* s1[4];   // second source (nullptr: one-term copy / scaling)
+    std::uint64_t ld0, ld1;
+    double sa, sb;         // residues in [0, p)
+    std::uint32_t on, writeback;
+};
+
 struct FramePrepParams {
     FrameQuads A, B, C;
+    FrameFold fold[2];               // 0: A, 1: B
     void* plane[PL_COUNT];           // nullptr: not materialised (raw blocks only)
     std::uint64_t pld[PL_COUNT];     // plane row pitch: uint16 elements, or bytes if limbs
     std::uint32_t limbs;             // 1: limb-pair planes (hi bytes [0,c), lo [c,2c) per row)

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <list>
 #include <map>
@@ -85,6 +86,40 @@ void op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) {
             if (h->rows) wr.push_back(*h);
 }
 
+// Read / write sets of the three launches of a fused frame (lower_frame).  Only
+// the prep reads the frame's operands: once it is done, the parent schedule's
+// next additions (which overwrite the temporaries holding this frame's A / B)
+// may run beside the GEMM and the combine.
+//   prep:    reads A, B, C (C_in);  writes the plane hosts in C, and (accumulating
+//            frames) raw planes in the third temporary / the spare h1 slot
+//   GEMM:    reads the planes in C (accumulating: also h1 / h2 and the float64
+//            B22 fallback in B);  writes the product planes in h0, h1
+//   combine: reads h0, h1 and the packed beta*C_in in C;  writes C
+void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size_t first) {
+    const bool acc = !f.is_zero(o.sb);
+    auto add = [](std::vector<View>& s, const View& v) {
+        if (v.rows) s.push_back(v);
+    };
+    for (std::size_t j = first; j < steps.size(); ++j) {
+        Step& s = steps[j];
+        if (std::getenv("WM_OLD_SETS")) { op_sets(o, s.rd, s.wr); continue; }
+        switch (s.kind) {
+            case Step::FPREP:
+                add(s.rd, o.a), add(s.rd, o.b), add(s.rd, o.d), add(s.wr, o.d);
+                if (acc) add(s.wr, o.h1), add(s.wr, o.h2);
+                break;
+            case Step::FGEMM:
+                add(s.rd, o.d), add(s.wr, o.h0), add(s.wr, o.h1);
+                if (acc) add(s.rd, o.a), add(s.rd, o.b), add(s.rd, o.h2);
+                break;
+            case Step::FCOMB:
+                add(s.rd, o.h0), add(s.rd, o.h1), add(s.rd, o.d), add(s.wr, o.d);
+                break;
+            default: op_sets(o, s.rd, s.wr);
+        }
+    }
+}
+
 bool sets_conflict(const Step& a, const Step& b) {
     auto hit = [](const std::vector<View>& x, const std::vector<View>& y) {
         for (const View& u : x)
@@ -144,6 +179,7 @@ struct wm_ctx {
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
     int dag = 4;                // concurrent issue over this many streams (0/1: one stream)
+    bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
                                 // SM ingress, not L2 or the issuing TMA unit, bounds the load)
     Lanes lanes;
@@ -240,12 +276,23 @@ void init_batch(AddBatch& b, const Field& f) {
     b.pinv = 1.0 / static_cast<double>(f.p);
 }
 
-int find_group(const Op& op) {
+// The fused group (gen_fusion.py) for the run starting at plan op i: the
+// longest one whose instructions are all still to be launched (a run whose
+// operand-producing additions were folded into the next frame's prep uses the
+// group generated for its remainder).
+int find_group(const Plan& plan, std::size_t i, const std::vector<char>& folded) {
+    const Op& op = plan.ops[i];
     if (op.frame < 0 || !op.sched) return -1;
-    for (int g = 0; g < fused::kNumGroups; ++g)
-        if (fused::kGroups[g].row0 == op.row && std::strcmp(fused::kGroups[g].sched, op.sched) == 0)
-            return g;
-    return -1;
+    int best = -1;
+    for (int g = 0; g < fused::kNumGroups; ++g) {
+        const fused::GroupDesc& G = fused::kGroups[g];
+        if (G.row0 != op.row || std::strcmp(G.sched, op.sched) != 0) continue;
+        if (i + G.nins > plan.ops.size()) continue;
+        bool clear = true;
+        for (int j = 0; j < G.nins; ++j) clear = clear && !(i + j < folded.size() && folded[i + j]);
+        if (clear && (best < 0 || G.nins > fused::kGroups[best].nins)) best = g;
+    }
+    return best;
 }
 
 // Bind the run of operations starting at ops[i] to fused group g: the rows must
@@ -465,6 +512,168 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     steps.push_back(cb);
 }
 
+// ---- folding a frame's operand additions into its prep ----------------------
+//
+// In the parent schedule a fused frame is usually preceded by the run of
+// additions that forms its operands (std2 rows 1-2: S3 -> X, T3 -> Y, then
+// P7 = X Y).  The prep can compute those operands from the run's sources
+// itself, saving the run's launch and its round trip through HBM; it stores the
+// operand back only when a later operation still reads it.
+
+struct Fold {
+    int op[2] = {-1, -1};  // plan op producing the frame's A / B
+    bool writeback[2] = {true, true};
+};
+
+bool is_add(const Op& o) { return o.kind == OP_ADDSUB || o.kind == OP_COPY; }
+
+void plan_op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) { op_sets(o, rd, wr); }
+
+bool any_overlap(const std::vector<View>& xs, const View& v) {
+    for (const View& x : xs)
+        if (x.rows && x.phys_overlaps(v)) return true;
+    return false;
+}
+
+// Is v read again after ops[i] before it is fully overwritten?
+bool live_after(const Plan& plan, std::size_t i, const View& v) {
+    for (std::size_t k = i + 1; k < plan.ops.size(); ++k) {
+        const Op& o = plan.ops[k];
+        std::vector<View> rd, wr;
+        op_sets(o, rd, wr);
+        if (any_overlap(rd, v)) return true;
+        if (any_overlap(wr, v)) return !(is_add(o) && o.d.same_window(v));
+    }
+    return v.region != R_T;  // caller-visible memory keeps its value
+}
+
+// Does a fused-addition group exist for exactly the plan ops [i, i + n)?
+bool group_exists(const Plan& plan, std::size_t i, std::size_t n) {
+    const Op& o = plan.ops[i];
+    if (!o.sched) return false;
+    for (int g = 0; g < fused::kNumGroups; ++g)
+        if (fused::kGroups[g].row0 == o.row && fused::kGroups[g].nins == static_cast<int>(n) &&
+            std::strcmp(fused::kGroups[g].sched, o.sched) == 0)
+            return true;
+    return false;
+}
+
+std::vector<Fold> plan_folds(const Plan& plan) {
+    std::vector<Fold> folds(plan.ops.size());
+    auto srcs = [](const Op& o) {
+        std::vector<View> v = {o.a};
+        if (o.kind == OP_ADDSUB) v.push_back(o.b);
+        return v;
+    };
+    for (std::size_t i = 0; i < plan.ops.size(); ++i) {
+        const Op& F = plan.ops[i];
+        if (F.kind != OP_FRAME || F.frame < 0 || F.a.phys_overlaps(F.b)) continue;
+        // the complete run of the parent's additions just before the frame
+        std::size_t j0 = i;
+        while (j0 > 0 && is_add(plan.ops[j0 - 1]) && plan.ops[j0 - 1].frame == F.frame) --j0;
+        if (std::getenv("WM_FOLD_DUMP")) {
+            std::fprintf(stderr, "frame %s/%d run %zu:", F.sched ? F.sched : "-", F.row, i - j0);
+            for (std::size_t j = j0; j < i; ++j)
+                std::fprintf(stderr, " %d%s", plan.ops[j].row,
+                             plan.ops[j].d.same_window(F.a) ? "a" : plan.ops[j].d.same_window(F.b) ? "b" : "-");
+            std::fprintf(stderr, "\n");
+        }
+        if (j0 == i) continue;
+        const bool acc = F.sb.r != 0;
+        // what the prep itself writes (the GEMM's product planes in h0 / h1 come later)
+        std::vector<View> prep_writes = {F.d};
+        if (acc) prep_writes.push_back(F.h1), prep_writes.push_back(F.h2);
+        // candidates: the last writer of each operand, if it writes exactly that
+        // operand and may move past the run's later instructions (none reads or
+        // writes its destination or writes its sources)
+        Fold fd;
+        for (int w = 0; w < 2; ++w) {
+            const View& X = w ? F.b : F.a;
+            std::size_t last = i;
+            for (std::size_t j = j0; j < i; ++j)
+                if (plan.ops[j].d.phys_overlaps(X)) last = j;
+            if (last == i || !plan.ops[last].d.same_window(X)) continue;
+            const Op& o = plan.ops[last];
+            bool ok = true;
+            for (const View& v : srcs(o)) {
+                // per-position ownership: a source is the operand itself or disjoint from it
+                if (!v.same_window(o.d) && v.phys_overlaps(o.d)) ok = false;
+                if (any_overlap(prep_writes, v)) ok = false;
+            }
+            for (std::size_t j = last + 1; j < i && ok; ++j) {
+                const Op& r = plan.ops[j];
+                if (r.d.phys_overlaps(o.d) || any_overlap(srcs(r), o.d) || any_overlap(srcs(o), r.d))
+                    ok = false;
+            }
+            if (ok) fd.op[w] = static_cast<int>(last);
+        }
+        // both folded: computed side by side from the state before either
+        if (fd.op[0] >= 0 && fd.op[1] >= 0) {
+            const Op& x = plan.ops[fd.op[0]];
+            const Op& y = plan.ops[fd.op[1]];
+            if (any_overlap(srcs(x), y.d) || any_overlap(srcs(y), x.d)) fd.op[1] = -1;
+        }
+        // an accumulating prep writes raw planes into h1 / h2: keep them off the operands
+        if (acc && (any_overlap({F.h1, F.h2}, F.a) || any_overlap({F.h1, F.h2}, F.b))) continue;
+        // the rest of the run must stay one launch: a contiguous fused group or a
+        // single addition (else folding would split a fused run into a chain)
+        auto rest_ok = [&](const Fold& f) {
+            std::vector<std::size_t> rest;
+            for (std::size_t j = j0; j < i; ++j)
+                if (static_cast<int>(j) != f.op[0] && static_cast<int>(j) != f.op[1]) rest.push_back(j);
+            if (rest.size() <= 1) return true;
+            if (rest.back() - rest.front() + 1 != rest.size()) return false;
+            return group_exists(plan, rest.front(), rest.size());
+        };
+        if (!rest_ok(fd)) {
+            Fold a = fd, b = fd;
+            a.op[1] = -1;
+            b.op[0] = -1;
+            fd = (a.op[0] >= 0 && rest_ok(a)) ? a : (b.op[1] >= 0 && rest_ok(b)) ? b : Fold();
+        }
+        if (fd.op[0] < 0 && fd.op[1] < 0) continue;
+        for (int w = 0; w < 2; ++w)
+            if (fd.op[w] >= 0) fd.writeback[w] = live_after(plan, i, w ? F.b : F.a);
+        // an accumulating frame with two temporaries has no plane slot left for
+        // B22: its GEMM reads that block of B as float64 (lower_frame)
+        if (acc && !F.h2.rows) fd.writeback[1] = true;
+        if (std::getenv("WM_FOLD_DUMP"))
+            std::fprintf(stderr, "  -> fold a=%d(wb %d) b=%d(wb %d) acc=%d h2=%d\n",
+                         fd.op[0] >= 0 ? plan.ops[fd.op[0]].row : 0, (int)fd.writeback[0],
+                         fd.op[1] >= 0 ? plan.ops[fd.op[1]].row : 0, (int)fd.writeback[1], (int)acc,
+                         (int)(F.h2.rows != 0));
+        folds[i] = fd;
+    }
+    return folds;
+}
+
+void apply_fold(const Plan& plan, const Fold& fd, double* const base[4], Step& prep) {
+    const Field& f = plan.field;
+    for (int w = 0; w < 2; ++w) {
+        FrameFold& ff = prep.fprep.fold[w];
+        std::memset(&ff, 0, sizeof(ff));
+        if (fd.op[w] < 0) continue;
+        const Op& o = plan.ops[fd.op[w]];
+        const auto q0 = quad_split(o.a);
+        for (int k = 0; k < 4; ++k) ff.s0[k] = base[q0[k].region] + q0[k].off;
+        ff.ld0 = o.a.ld;
+        if (o.kind == OP_ADDSUB) {
+            const auto q1 = quad_split(o.b);
+            for (int k = 0; k < 4; ++k) ff.s1[k] = base[q1[k].region] + q1[k].off;
+            ff.ld1 = o.b.ld;
+            ff.sb = static_cast<double>(o.sb.r);
+        }
+        ff.sa = static_cast<double>(o.sa.r);
+        ff.on = 1;
+        ff.writeback = fd.writeback[w] ? 1 : 0;
+        // dependency sets: the sources are read, the operand view is (re)written
+        prep.rd.push_back(o.a);
+        if (o.kind == OP_ADDSUB) prep.rd.push_back(o.b);
+        prep.wr.push_back(o.d);
+    }
+    (void)f;
+}
+
 // Lower an operation list to launches.  Additions are merged into one launch
 // while they are pairwise independent (no write of one touches a read or
 // write of another) and contiguous in program order.
@@ -506,10 +715,17 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         return false;
     };
+    const bool fold = ctx.fold && !f.real;
+    const std::vector<Fold> folds = fold ? plan_folds(plan) : std::vector<Fold>();
+    std::vector<char> folded(plan.ops.size(), 0);
+    for (const Fold& fd : folds)
+        for (int w = 0; w < 2; ++w)
+            if (fd.op[w] >= 0) folded[fd.op[w]] = 1;
     for (std::size_t oi = 0; oi < plan.ops.size(); ++oi) {
         const Op& op = plan.ops[oi];
+        if (folded[oi]) continue;  // computed by the next frame's prep
         if ((op.kind == OP_ADDSUB || op.kind == OP_COPY) && ctx.fuse_adds) {
-            const int g = find_group(op);
+            const int g = find_group(plan, oi, folded);
             Step gs{};
             if (g >= 0 && try_group(plan, oi, g, base, gs)) {
                 flush();
@@ -530,7 +746,10 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             const std::size_t first = steps.size();
             lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
                         ctx.direct_ok && ctx.direct_frames, ctx.multicast);
-            for (std::size_t j = first; j < steps.size(); ++j) op_sets(op, steps[j].rd, steps[j].wr);
+            frame_sets(op, f, steps, first);
+            if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
+                for (std::size_t j = first; j < steps.size(); ++j)
+                    if (steps[j].kind == Step::FPREP) apply_fold(plan, folds[oi], base, steps[j]);
             continue;
         }
         Step s{};
@@ -778,6 +997,10 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                 for (int i = 0; i < PL_COUNT; ++i) planes += s.fprep.plane[i] != nullptr;
                 r->frame_prep_bytes += (8 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double) +
                                        planes * c2 * 2 + (s.fprep.beta ? c2 * 8 : 0);
+                for (const FrameFold& ff : s.fprep.fold)  // folded operands: second source, store
+                    if (ff.on)
+                        r->frame_prep_bytes += ((ff.s1[0] ? 4 : 0) + (ff.writeback ? 4 : 0)) * c2 *
+                                               sizeof(double);
             }
             if (s.kind == Step::FCOMB) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fcomb.c) * s.fcomb.c;
@@ -829,7 +1052,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -852,13 +1075,18 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
         cp = ctx->cache.front().second.get();
     }
-    const bool dag = ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1;
+    // concurrent issue pays only for launches of real size; tiny problems (deep
+    // recursions of the unit tests) would spend more on the dependency analysis
+    const bool dag = ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1 &&
+                     std::max({A.rows, A.cols, B.cols}) >= 512 && cp->steps.size() <= 200000;
     if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps, ctx->dag));
     auto go = [&]() {
         if (dag) issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes, ctx->dag);
         else issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
     };
-    if (ctx->graphs && cp->steps.size() > 1) {
+    // capture pays for the launch-bound plans of real problems; the 10^5-launch
+    // plans of unit-size recursions (cutoff 1) are cheaper to issue directly
+    if (ctx->graphs && cp->steps.size() > 1 && cp->steps.size() <= 50000) {
         if (!cp->exec) {
             WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
             try {
@@ -1011,6 +1239,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "dag") ctx->dag = static_cast<int>(value);
         else if (k == "pdl") g_pdl_user = value != 0;
         else if (k == "multicast") ctx->multicast = value != 0;
+        else if (k == "fold") ctx->fold = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -1031,6 +1260,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "dag") *value = ctx->dag;
         else if (k == "pdl") *value = g_pdl_user;
         else if (k == "multicast") *value = ctx->multicast;
+        else if (k == "fold") *value = ctx->fold;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
@@ -1262,6 +1492,31 @@ int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, in
         // kinds of the launches off lane 0: ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
         for (std::size_t j = 0; j < steps.size(); ++j)
             if (d.lane[j] != 0) out[10 + steps[j].kind] += 1;
+        // launch-level DAG (the read / write sets the concurrent issue uses), cost
+        // model per launch kind in microseconds (measured C2 means):
+        // ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
+        const double kc[7] = {2.5, 6.0, 9.0, 2.5, 2.8, 4.1, 2.0};
+        const std::size_t S = steps.size();
+        std::vector<double> sfin(S, 0.0);
+        double stot = 0, scrit = 0;
+        for (std::size_t j = 0; j < S; ++j) {
+            double start = 0;
+            for (std::size_t i = j; i-- > 0;) {
+                if (sfin[i] <= start) continue;
+                if (sets_conflict(steps[i], steps[j])) start = std::max(start, sfin[i]);
+            }
+            sfin[j] = start + kc[steps[j].kind];
+            stot += kc[steps[j].kind];
+            scrit = std::max(scrit, sfin[j]);
+        }
+        out[20] = stot;
+        out[21] = scrit;
+        for (const Step& st : steps)
+            if (st.kind == Step::FPREP)
+                for (const FrameFold& ff : st.fprep.fold) {
+                    out[22] += ff.on;
+                    out[23] += ff.on && ff.writeback;
+                }
         if (std::getenv("WM_DAG_DUMP"))
             for (std::size_t j = 0; j < steps.size() && j < 400; ++j)
                 std::fprintf(stderr, "%zu lane %d kind %d waits %zu\n", j, d.lane[j], steps[j].kind,

@@ -43,7 +43,8 @@ def programs():
 
 
 def parse(prog):
-    """-> list of (row, kind, dst, operands) with kind in add/copy/product."""
+    """-> list of (row, kind, dst, operands) with kind in add/copy/product
+    (a product's operands are its two factor slots)."""
     out = []
     row = 0
     for raw in prog.splitlines():
@@ -57,7 +58,8 @@ def parse(prog):
         if rhs and rhs[0].endswith(":"):
             rhs = rhs[1:]
         if "*" in rhs:
-            out.append((row, "product", dst, []))
+            k = rhs.index("*")
+            out.append((row, "product", dst, [rhs[k - 1].lstrip("("), rhs[k + 1].rstrip(")")]))
             continue
         ops = [t for t in rhs if t in SLOTS]
         out.append((row, "add" if len(ops) == 2 else "copy", dst, ops))
@@ -78,10 +80,51 @@ def runs(ins):
     return res
 
 
+def fold_remainders(ins):
+    """Runs left behind when a leaf frame folds the additions producing its
+    operands into its prep (wm_runtime.cu plan_folds): for every run followed by
+    a product, the last writer of each factor slot may move into the product if
+    no later instruction of the run reads or writes its destination or writes
+    its sources.  Returns the contiguous remainders of >= 2 instructions."""
+    out = []
+    cur = []
+    for r in ins:
+        if r[1] != "product":
+            cur.append(r)
+            continue
+        run, cur = cur, []
+        if not run:
+            continue
+        folded = []
+        for slot in r[3]:
+            last = max((i for i, x in enumerate(run) if x[2] == slot), default=None)
+            if last is None or last in folded:
+                continue
+            f = run[last]
+            ok = all(f[2] not in x[3] and x[2] != f[2] and x[2] not in f[3]
+                     for x in run[last + 1:])
+            if ok:
+                folded.append(last)
+        if len(folded) == 2:  # the two folded instructions are computed together
+            a, b = (run[i] for i in folded)
+            if a[2] in b[3] or b[2] in a[3]:
+                folded = folded[:1]
+        rest = [x for i, x in enumerate(run) if i not in folded]
+        if folded and len(rest) >= 2 and rest[-1][0] - rest[0][0] == len(rest) - 1:
+            out.append(rest)
+    return out
+
+
 def main():
     groups = []
     for name, prog in programs().items():
-        for run in runs(parse(prog)):
+        ins = parse(prog)
+        seen = set()
+        for run in runs(ins) + fold_remainders(ins):
+            key = (run[0][0], len(run))
+            if key in seen:
+                continue
+            seen.add(key)
             slots, loads, stores = [], [], []
             for (_, _, dst, ops) in run:
                 for s in ops:

@@ -43,14 +43,15 @@ def golden():
 
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
                         dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
-                        dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0), dict(multicast=1)],
+                        dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0), dict(multicast=1),
+                        dict(fold=0)],
                 ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync", "convert-frames",
-                     "one-stream", "multicast"])
+                     "one-stream", "multicast", "no-fold"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
                                               "leaf_kernel", "fuse_adds", "gemm_engine",
-                                              "direct_frames", "dag", "multicast")}
+                                              "direct_frames", "dag", "multicast", "fold")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
@@ -68,8 +69,8 @@ def test_device_generator_matches_fill_random(W, O):
 def test_golden_small_cases(W, golden, options):
     seen = 0
     for c in golden:
-        if c["seed"] != 11 and options:
-            continue  # option sweeps replay one seed; the default replays all
+        if options and (c["seed"] != 11 or c["cutoff"] == 1):
+            continue  # option sweeps replay one seed above unit cutoff; the default replays all
         v, m, k, n = c["variant"], c["m"], c["k"], c["n"]
         A, B, C = _problem(W, m, k, n, c["seed"], _acc(v))
         if "error" in c:
@@ -87,7 +88,7 @@ def test_golden_small_cases(W, golden, options):
         assert rep.mults == c["report"]["mults"] and rep.adds == c["report"]["adds"]
         assert rep.peak_extra_words == c["report"]["peak_extra_words"]
         seen += 1
-    assert seen > 300
+    assert seen > (300 if not options else 100)
 
 
 def test_primitive_kats(W):
@@ -130,14 +131,18 @@ def test_classical_vs_oracle_random_shapes(W, O, options):
                                "ipmm", "iprect"])
 def test_midsize_vs_oracle(W, O, v, options):
     """512..1024-sized problems at cutoffs 64/128 vs the oracle classical product."""
-    for (m, k, n, c) in [(512, 512, 512, 64), (1024, 1024, 1024, 128)]:
+    cases = [(512, 512, 512, 64, 1), (1024, 1024, 1024, 128, 1)]
+    if v not in ("ipmm", "iprect"):  # general scalars through fused / folded frames
+        cases.append((1024, 1024, 1024, 128, 3))
+    for (m, k, n, c, al) in cases:
         if v == "iprect":
             m, n = 2 * m, 2 * n
-        A, B, C = _problem(W, m, k, n, 101 + m, _acc(v))
+        be = (1 if al == 1 else 7) if _acc(v) else 0
+        A, B, C = _problem(W, m, k, n, 101 + m + al, _acc(v))
         a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
-        W.run_variant(v, A, B, C, alpha=1, beta=1 if _acc(v) else 0, cutoff=c)
-        want = O.classical_modp(a0, b0, c0 if _acc(v) else None, 1, 1 if _acc(v) else 0)
-        assert (C.to_u32() == want).all(), (v, m, k, n, c, options)
+        W.run_variant(v, A, B, C, alpha=al, beta=be, cutoff=c)
+        want = O.classical_modp(a0, b0, c0 if _acc(v) else None, al, be)
+        assert (C.to_u32() == want).all(), (v, m, k, n, c, al, be, options)
 
 
 CFG = json.load(open(os.path.join(GOLD, "config_hashes.json")))
