@@ -42,6 +42,7 @@ struct AddBatch {
     int n;
     std::uint32_t p;
     double pd, pinv;
+    unsigned long long* tl;  // measurement timeline slot (nullptr: off)
 };
 
 // C <- alpha*A*B + beta*C on one leaf (or one fused frame).
@@ -55,6 +56,7 @@ struct MulParams {
     double alphad, betad;       // values (REAL64)
     std::uint32_t p;
     double pd, pinv;
+    unsigned long long* tl;  // measurement timeline slot (nullptr: off)
 };
 
 // kernels (wm_kernels.cu, wm_dmma.cu, wm_i8.cu, wm_frame.cu)

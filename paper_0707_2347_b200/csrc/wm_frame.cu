@@ -24,72 +24,16 @@
 
 #include "wm_launch.h"
 #include "wm_frame.h"
+#include "wm_frame_dev.cuh"
 
 namespace wm {
 namespace {
 
-__device__ __forceinline__ double rmod(double v, double p, double pinv) {
-    const double q = floor(v * pinv);
-    double r = fma(-q, p, v);
-    r = r < 0.0 ? r + p : r;
-    return r >= p ? r - p : r;
-}
-__device__ __forceinline__ double addm(double a, double b, double p) {
-    const double v = a + b;
-    return v >= p ? v - p : v;
-}
-__device__ __forceinline__ double subm(double a, double b, double p) {
-    const double v = a - b;
-    return v < 0.0 ? v + p : v;
-}
-
-__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
-    const double2 a = *reinterpret_cast<const double2*>(p);
-    const double2 b = *reinterpret_cast<const double2*>(p + 2);
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = b.x;
-    v[3] = b.y;
-}
-
-__device__ __forceinline__ uint2 pack(double a, double b, double c, double d) {
-    return make_uint2(static_cast<std::uint32_t>(a) | (static_cast<std::uint32_t>(b) << 16),
-                      static_cast<std::uint32_t>(c) | (static_cast<std::uint32_t>(d) << 16));
-}
-
-// The four quadrant values (row r, columns j, j+1) of a frame operand: loaded
-// from its view, or -- folded -- computed from the sources of the parent
-// addition(s) that produce it (sa*s0 + sb*s1 < 2^33: exact, one reduction).
-__device__ __forceinline__ void load_operand(const FrameQuads& X, const FrameFold& F,
-                                             std::uint64_t r, std::uint64_t j, double p,
-                                             double pinv, double (&v)[4][2]) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (!F.on) {
-            const double2 x = *reinterpret_cast<const double2*>(X.q[k] + r * X.ld + j);
-            v[k][0] = x.x;
-            v[k][1] = x.y;
-            continue;
-        }
-        const double2 a = *reinterpret_cast<const double2*>(F.s0[k] + r * F.ld0 + j);
-        double2 b = make_double2(0.0, 0.0);
-        if (F.s1[0]) b = *reinterpret_cast<const double2*>(F.s1[k] + r * F.ld1 + j);
-        v[k][0] = rmod(fma(F.sa, a.x, F.sb * b.x), p, pinv);
-        v[k][1] = rmod(fma(F.sa, a.y, F.sb * b.y), p, pinv);
-    }
-}
-
-// Store a folded operand into its own view when a later operation reads it.
-// Every position is written by the thread that read it (the sources are either
-// this view itself, same window, or disjoint from it).
-__device__ __forceinline__ void store_operand(const FrameQuads& X, const FrameFold& F,
-                                              std::uint64_t r, std::uint64_t j,
-                                              const double (&v)[4][2]) {
-    if (!F.on || !F.writeback) return;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        *reinterpret_cast<double2*>(X.q[k] + r * X.ld + j) = make_double2(v[k][0], v[k][1]);
-}
+using fdev::rmod;
+using fdev::addm;
+using fdev::subm;
+using fdev::load_operand;
+using fdev::store_operand;
 
 // thread (r, q, h), q < c/4, h in {0,1}: plane columns j = 4q + 2h, +1; the
 // float64 slots (r, q + k c/4), k = 0..3, of every host / C block are owned by
@@ -98,6 +42,7 @@ __device__ __forceinline__ void store_operand(const FrameQuads& X, const FrameFo
 __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
+    WM_TL_BEGIN(P.tl);
     const std::uint32_t c4 = P.c / 4;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     const bool live = idx < static_cast<std::uint64_t>(P.c) * c4 * 2;
@@ -164,6 +109,7 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
             *reinterpret_cast<std::uint32_t*>(c11 + 4 * (r * P.C.ld + q + k * c4) + 2 * h) =
                 static_cast<std::uint32_t>(cin[k][0]) | (static_cast<std::uint32_t>(cin[k][1]) << 16);
     }
+    WM_TL_END(P.tl);
     WM_PDL_LATE_M();
 }
 
@@ -175,74 +121,13 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
 __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
+    WM_TL_BEGIN(P.tl);
     const std::uint64_t r = blockIdx.x, j = 2 * threadIdx.x;
-    const double p = P.pd, pinv = P.pinv;
-    double av[4][2], bv[4][2];
-    double(&a11)[2] = av[0], (&a12)[2] = av[1], (&a21)[2] = av[2], (&a22)[2] = av[3];
-    double(&b11)[2] = bv[0], (&b12)[2] = bv[1], (&b21)[2] = bv[2], (&b22)[2] = bv[3];
-    load_operand(P.A, P.fold[0], r, j, p, pinv, av);
-    load_operand(P.B, P.fold[1], r, j, p, pinv, bv);
-    auto ld2 = [&](const double* ptr, double (&v)[2]) {
-        const double2 x = *reinterpret_cast<const double2*>(ptr);
-        v[0] = x.x;
-        v[1] = x.y;
-    };
-    double cin[4][2];  // [quadrant][column]
-    if (P.beta != 0) {
-        const double be = static_cast<double>(P.beta);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            double v[2];
-            ld2(P.C.q[k] + r * P.C.ld + j, v);
-            cin[k][0] = rmod(be * v[0], p, pinv);
-            cin[k][1] = rmod(be * v[1], p, pinv);
-        }
-    }
+    fdev::PrepRegs R;
+    fdev::prep_limbs_load(P, r, j, R);
     __syncthreads();  // row r of every host has been read before any of it is overwritten
-    store_operand(P.A, P.fold[0], r, j, av);
-    store_operand(P.B, P.fold[1], r, j, bv);
-    double s[4][2], t[4][2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const double s1 = addm(a21[e], a22[e], p), s2 = subm(s1, a11[e], p);
-        s[0][e] = s1;
-        s[1][e] = s2;
-        s[2][e] = subm(a11[e], a21[e], p);
-        s[3][e] = subm(a12[e], s2, p);
-        const double t1 = subm(b12[e], b11[e], p), t2 = subm(b22[e], t1, p);
-        t[0][e] = t1;
-        t[1][e] = t2;
-        t[2][e] = subm(b22[e], b12[e], p);
-        t[3][e] = subm(t2, b21[e], p);
-    }
-    const std::uint32_t c = P.c;
-    auto put = [&](int pl, const double (&v)[2]) {
-        if (!P.plane[pl]) return;
-        std::uint8_t* row = static_cast<std::uint8_t*>(P.plane[pl]) + r * P.pld[pl];
-        const std::uint32_t x0 = static_cast<std::uint32_t>(v[0]), x1 = static_cast<std::uint32_t>(v[1]);
-        *reinterpret_cast<std::uint16_t*>(row + j) = static_cast<std::uint16_t>((x0 >> 8) | (x1 & 0xFF00u));
-        *reinterpret_cast<std::uint16_t*>(row + c + j) =
-            static_cast<std::uint16_t>((x0 & 255u) | ((x1 & 255u) << 8));
-    };
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        put(PL_S1 + k, s[k]);
-        put(PL_T1 + k, t[k]);
-    }
-    put(PL_A11, a11);
-    put(PL_A12, a12);
-    put(PL_A22, a22);
-    put(PL_B11, b11);
-    put(PL_B21, b21);
-    put(PL_B22, b22);
-    if (P.beta != 0) {
-        std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]) + 4 * (r * P.C.ld + j);
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-            reinterpret_cast<uint2*>(c11)[e] = make_uint2(
-                static_cast<std::uint32_t>(cin[0][e]) | (static_cast<std::uint32_t>(cin[1][e]) << 16),
-                static_cast<std::uint32_t>(cin[2][e]) | (static_cast<std::uint32_t>(cin[3][e]) << 16));
-    }
+    fdev::prep_limbs_store(P, r, j, R);
+    WM_TL_END(P.tl);
     WM_PDL_LATE_M();
 }
 
@@ -250,49 +135,14 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
 __global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
+    WM_TL_BEGIN(P.tl);
     const std::uint32_t c2 = P.c / 2;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= static_cast<std::uint64_t>(P.c) * c2) return;
-    const std::uint64_t r = idx / c2, j = 2 * (idx - r * c2);
-    const double p = P.pd, pinv = P.pinv;
-    double pv[7][2];
-#pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        const std::uint32_t w = *reinterpret_cast<const std::uint32_t*>(P.P[k] + r * P.pld[k] + j);
-        pv[k][0] = static_cast<double>(w & 0xFFFFu);
-        pv[k][1] = static_cast<double>(w >> 16);
+    if (idx < static_cast<std::uint64_t>(P.c) * c2) {
+        const std::uint64_t r = idx / c2, j = 2 * (idx - r * c2);
+        fdev::comb_pair<false>(P, r, j);
     }
-    double cin[2][4];  // [col e][quadrant]
-    if (P.beta != 0) {
-        const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const uint2 w = *reinterpret_cast<const uint2*>(c11 + 4 * (r * P.C.ld + j + e));
-            cin[e][0] = static_cast<double>(w.x & 0xFFFFu);
-            cin[e][1] = static_cast<double>(w.x >> 16);
-            cin[e][2] = static_cast<double>(w.y & 0xFFFFu);
-            cin[e][3] = static_cast<double>(w.y >> 16);
-        }
-    }
-    const double al = static_cast<double>(P.alpha);
-    double out[4][2];  // [quadrant][col]
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const double p1 = pv[0][e], p2 = pv[1][e], p3 = pv[2][e], p4 = pv[3][e],
-                     p5 = pv[4][e], p6 = pv[5][e], p7 = pv[6][e];
-        const double u2 = p1 + p6;
-        const double u3 = u2 + p7;
-        const double u[4] = {p1 + p2, u2 + p5 + p3, u3 + (p - p4), u3 + p5};  // < 4p
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-            double v = rmod(u[qd], p, pinv) * al;
-            if (P.beta != 0) v += cin[e][qd];
-            out[qd][e] = rmod(v, p, pinv);
-        }
-    }
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd)
-        *reinterpret_cast<double2*>(P.C.q[qd] + r * P.C.ld + j) = make_double2(out[qd][0], out[qd][1]);
+    WM_TL_END(P.tl);
     WM_PDL_LATE_M();
 }
 

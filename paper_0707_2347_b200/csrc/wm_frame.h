@@ -38,6 +38,7 @@ struct FramePrepParams {
     std::uint32_t c;                 // quadrant size
     std::uint32_t beta;              // accumulate: pack beta*C_in into C11 slots
     double pd, pinv;
+    unsigned long long* tl;          // measurement timeline slot (nullptr: off)
 };
 
 struct FrameCombParams {
@@ -47,9 +48,20 @@ struct FrameCombParams {
     std::uint32_t c;
     std::uint32_t alpha, beta;  // beta != 0: packed beta*C_in in the C11 slots
     double pd, pinv;
+    unsigned long long* tl;     // measurement timeline slot (nullptr: off)
 };
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s);
+
+// One fused frame in a single cooperative launch (wm_direct.cu): prep, the
+// seven-product direct GEMM and the combine as phases between grid barriers;
+// `bar` is the launch's zero-initialised {count, sense} pair.
+struct GemmParams;
+struct TmaMaps;
+bool frame_coop_supported(const GemmParams& G, int bn);
+cudaError_t launch_frame_coop(const FramePrepParams& PP, const GemmParams& GP,
+                              const FrameCombParams& CP, const TmaMaps& M, int bn,
+                              std::uint32_t* bar, cudaStream_t s);
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s);
 
 }  // namespace wm

@@ -6,5 +6,6 @@
 #include "wm_fused_gen.cuh"
 
 namespace wm {
-cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s);
+cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s,
+                         unsigned long long* tl = nullptr);
 }  // namespace wm

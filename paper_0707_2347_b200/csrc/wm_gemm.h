@@ -28,6 +28,7 @@ struct GemmParams {
     double pd, pinv;
     unsigned long long* trace;  // diagnostics: per-CTA phase timestamps (nullptr: off)
     std::uint32_t mc_n, mc_m;   // direct engine: TMA-multicast cluster extent along N / M tiles
+    unsigned long long* tl;     // measurement timeline slot (nullptr: off)
 };
 
 // TMA operand maps (one pair per product), encoded on the host at lowering time

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
     // next kernel in the chain start its launch
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
+    WM_TL_BEGIN(B.tl);
     int i = 0;
 #pragma unroll 1
     while (i + 1 < B.n && blockIdx.x >= B.it[i + 1].blk0) ++i;
@@ -107,6 +108,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
             t.d[rr * t.ldd + cc] = apply<REAL>(a, b, mode, sa, sb, p, pinv);
         }
     }
+    WM_TL_END(B.tl);
     WM_PDL_LATE_M();
 }
 
@@ -126,15 +128,19 @@ namespace {
 // position of the (identically shaped, pairwise disjoint) slot views and
 // executes the run's dataflow on registers -- each slot read once, written once.
 template <bool REAL>
-__global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams G) {
+__global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams G,
+                                                unsigned long long* tl) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
+    WM_TL_BEGIN(tl);
     const std::uint32_t cv = G.cols >> 1;
     const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * cv;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx >= total) return;
-    const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
-    fused::group_dispatch<REAL>(gid, G, r, c);
+    if (idx < total) {
+        const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
+        fused::group_dispatch<REAL>(gid, G, r, c);
+    }
+    WM_TL_END(tl);
     WM_PDL_LATE_M();
 }
 
@@ -226,7 +232,8 @@ cudaError_t launch_addsub(const AddBatch& b, bool real, unsigned blocks, cudaStr
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s) {
+cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaStream_t s,
+                         unsigned long long* tl) {
     const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * (G.cols / 2);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>((total + 255) / 256));
@@ -237,8 +244,8 @@ cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaSt
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G);
-    return cudaLaunchKernelEx(&cfg, k_group<false>, gid, G);
+    if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G, tl);
+    return cudaLaunchKernelEx(&cfg, k_group<false>, gid, G, tl);
 }
 
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,

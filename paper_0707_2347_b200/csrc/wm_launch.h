@@ -18,6 +18,25 @@ extern bool g_pdl;
 #ifndef WM_PDL_LATE_MEMORY
 #define WM_PDL_LATE_MEMORY 0
 #endif
+// Measurement timeline (the "trace" context option, wm_diag_trace): thread 0 of
+// every CTA folds %globaltimer into its launch's [first start, last end] slot.
+#define WM_TL_NOW(t_) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_))
+#define WM_TL_BEGIN(tl)                                       \
+    do {                                                      \
+        if ((tl) && threadIdx.x == 0) {                       \
+            unsigned long long t_;                            \
+            WM_TL_NOW(t_);                                    \
+            atomicMin((tl), t_);                              \
+        }                                                     \
+    } while (0)
+#define WM_TL_END(tl)                                         \
+    do {                                                      \
+        if ((tl) && threadIdx.x == 0) {                       \
+            unsigned long long t_;                            \
+            WM_TL_NOW(t_);                                    \
+            atomicMax((tl) + 1, t_);                          \
+        }                                                     \
+    } while (0)
 #define WM_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory")
 #if WM_PDL_LATE_COMPUTE
 #define WM_PDL_EARLY_C()

@@ -57,7 +57,7 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 struct Step {
-    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB } kind;
+    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB, FCOOP } kind;
     AddBatch add;
     unsigned blocks = 0;
     MulParams mul;
@@ -70,6 +70,8 @@ struct Step {
     int engine = 0;         // int8 GEMM: 0 cp.async, 1 TMA
     int bn = 32, split = 1;
     std::shared_ptr<TmaMaps> tmaps;
+    unsigned long long* tl = nullptr;  // GROUP: measurement timeline slot
+    std::uint32_t* bar = nullptr;      // FCOOP: the launch's grid-barrier pair
     // memory the launch reads / writes (dependency analysis for concurrent issue)
     std::vector<View> rd, wr;
 };
@@ -95,6 +97,8 @@ void op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) {
 //   GEMM:    reads the planes in C (accumulating: also h1 / h2 and the float64
 //            B22 fallback in B);  writes the product planes in h0, h1
 //   combine: reads h0, h1 and the packed beta*C_in in C;  writes C
+constexpr std::uint8_t kGridRegion = 200;  // pseudo region: "all SMs" (cooperative frames)
+
 void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size_t first) {
     const bool acc = !f.is_zero(o.sb);
     auto add = [](std::vector<View>& s, const View& v) {
@@ -115,6 +119,17 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
             case Step::FCOMB:
                 add(s.rd, o.h0), add(s.rd, o.h1), add(s.rd, o.d), add(s.wr, o.d);
                 break;
+            case Step::FCOOP: {
+                op_sets(o, s.rd, s.wr);
+                // one cooperative frame at a time: its grid needs every SM
+                View grid;
+                grid.region = kGridRegion;
+                grid.origin = 0;
+                grid.rows = grid.cols = grid.ld = 1;
+                s.rd.push_back(grid);
+                s.wr.push_back(grid);
+                break;
+            }
             default: op_sets(o, s.rd, s.wr);
         }
     }
@@ -138,7 +153,11 @@ struct CachedPlan {
     double* arena = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    unsigned long long* tl = nullptr;  // measurement timeline (trace option)
+    std::uint32_t* bars = nullptr;     // grid-barrier pairs of the cooperative frames
     ~CachedPlan() {
+        if (tl) cudaFree(tl);
+        if (bars) cudaFree(bars);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (arena) cudaFree(arena);
@@ -178,8 +197,12 @@ struct wm_ctx {
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
-    int dag = 4;                // concurrent issue over this many streams (0/1: one stream)
+    int dag = 2;                // concurrent issue over this many streams (0/1: one stream;
+                                // measured: 2 >= 3, 4, 6 > 8 lanes)
     bool fold = true;           // fold a frame's operand-producing additions into its prep
+    bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
+    bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
+    const void* traced = nullptr;  // CachedPlan of the last traced run
     bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
                                 // SM ingress, not L2 or the issuing TMA unit, bounds the load)
     Lanes lanes;
@@ -746,10 +769,21 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             const std::size_t first = steps.size();
             lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
                         ctx.direct_ok && ctx.direct_frames, ctx.multicast);
+            if (ctx.coop_frames && steps.size() == first + 3 && steps[first + 1].engine == 2 &&
+                frame_coop_supported(steps[first + 1].fgemm, steps[first + 1].bn)) {
+                // the three launches as phases of one cooperative launch
+                Step co = steps[first + 1];
+                co.kind = Step::FCOOP;
+                co.fprep = steps[first].fprep;
+                co.fcomb = steps[first + 2].fcomb;
+                steps.resize(first);
+                steps.push_back(co);
+            }
             frame_sets(op, f, steps, first);
             if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
                 for (std::size_t j = first; j < steps.size(); ++j)
-                    if (steps[j].kind == Step::FPREP) apply_fold(plan, folds[oi], base, steps[j]);
+                    if (steps[j].kind == Step::FPREP || steps[j].kind == Step::FCOOP)
+                        apply_fold(plan, folds[oi], base, steps[j]);
             continue;
         }
         Step s{};
@@ -785,6 +819,7 @@ bool long_step(const Step& s) {
         case Step::FPREP: return s.fprep.c >= 1024;
         case Step::FGEMM: return s.fgemm.m >= 1024;
         case Step::FCOMB: return s.fcomb.c >= 1024;
+        case Step::FCOOP: return s.fcomb.c >= 1024;
         default: return false;
     }
 }
@@ -816,7 +851,7 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
             }
             break;
         case Step::FRAME: break;
-        case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st)); break;
+        case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st, s.tl)); break;
         case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
         case Step::FGEMM:
             if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
@@ -824,6 +859,9 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
             else WM_CUDA(launch_gemm_i8(s.fgemm, st));
             break;
         case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
+        case Step::FCOOP:
+            WM_CUDA(launch_frame_coop(s.fprep, s.fgemm, s.fcomb, *s.tmaps, s.bn, s.bar, st));
+            break;
     }
 }
 
@@ -832,7 +870,8 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
     for (const Step& s : steps) {
         if (subset == 1 && s.kind != Step::ADD && s.kind != Step::GROUP) continue;
         if (subset == 2 && s.kind != Step::MUL) continue;
-        if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB)
+        if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB &&
+            s.kind != Step::FCOOP)
             continue;
         if (subset == 4 && s.kind != Step::FPREP) continue;
         if (subset == 5 && s.kind != Step::FGEMM) continue;
@@ -979,7 +1018,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                     r->add_bytes_issued += (s.add.it[i].mode <= M_GEN ? 3 : 2) *
                                            static_cast<std::uint64_t>(s.add.it[i].rows) *
                                            s.add.it[i].cols * sizeof(double);
-            if (s.kind == Step::FGEMM) {
+            if (s.kind == Step::FGEMM || s.kind == Step::FCOOP) {
                 const GemmParams& G = s.fgemm;
                 const std::uint64_t mk = static_cast<std::uint64_t>(G.m) * G.k,
                                     kn = static_cast<std::uint64_t>(G.k) * G.n,
@@ -990,7 +1029,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                                            kn * (G.b[i].fmt != 0 ? 2 : 8) +
                                            mn * (G.c[i].fmt != 0 ? 2 : 8);
             }
-            if (s.kind == Step::FPREP) {
+            if (s.kind == Step::FPREP || s.kind == Step::FCOOP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fprep.c) * s.fprep.c;
                 r->frame_bytes += (4 + 4 + 4 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double);
                 int planes = 0;
@@ -1002,7 +1041,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                         r->frame_prep_bytes += ((ff.s1[0] ? 4 : 0) + (ff.writeback ? 4 : 0)) * c2 *
                                                sizeof(double);
             }
-            if (s.kind == Step::FCOMB) {
+            if (s.kind == Step::FCOMB || s.kind == Step::FCOOP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fcomb.c) * s.fcomb.c;
                 r->frame_comb_bytes += 7 * c2 * 2 + (s.fcomb.beta ? c2 * 8 : 0) + 4 * c2 * sizeof(double);
             }
@@ -1052,7 +1091,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -1071,6 +1110,15 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
             WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
         double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
         np->steps = lower(np->plan, base, *ctx);
+        std::size_t ncoop = 0;
+        for (const Step& st : np->steps) ncoop += st.kind == Step::FCOOP;
+        if (ncoop) {  // zeroed {count, sense} per cooperative launch
+            WM_CUDA(cudaMalloc(&np->bars, 2 * ncoop * sizeof(std::uint32_t)));
+            WM_CUDA(cudaMemset(np->bars, 0, 2 * ncoop * sizeof(std::uint32_t)));
+            std::size_t i = 0;
+            for (Step& st : np->steps)
+                if (st.kind == Step::FCOOP) st.bar = np->bars + 2 * i++;
+        }
         ctx->cache.emplace_front(k, std::move(np));
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
         cp = ctx->cache.front().second.get();
@@ -1080,8 +1128,27 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     const bool dag = ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1 &&
                      std::max({A.rows, A.cols, B.cols}) >= 512 && cp->steps.size() <= 200000;
     if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps, ctx->dag));
+    if (ctx->trace) {
+        // [start, end] globaltimer slots per launch, patched into the launch
+        // parameters of this (trace-keyed) plan before its graph is captured
+        if (!cp->tl) {
+            WM_CUDA(cudaMalloc(&cp->tl, 2 * cp->steps.size() * sizeof(unsigned long long)));
+            for (std::size_t j = 0; j < cp->steps.size(); ++j) {
+                Step& st = cp->steps[j];
+                unsigned long long* slot = cp->tl + 2 * j;
+                st.add.tl = st.mul.tl = st.fprep.tl = st.fcomb.tl = st.fgemm.tl = st.tl = slot;
+            }
+        }
+        std::vector<unsigned long long> init(2 * cp->steps.size(), 0ull);
+        for (std::size_t j = 0; j < cp->steps.size(); ++j) init[2 * j] = ~0ull;
+        WM_CUDA(cudaMemcpyAsync(cp->tl, init.data(), init.size() * sizeof(unsigned long long),
+                                cudaMemcpyHostToDevice, ctx->stream));
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->traced = cp;
+    }
     auto go = [&]() {
-        if (dag) issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes, ctx->dag);
+        if (dag)
+            issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes, ctx->dag);
         else issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
     };
     // capture pays for the launch-bound plans of real problems; the 10^5-launch
@@ -1240,6 +1307,8 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "pdl") g_pdl_user = value != 0;
         else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
+        else if (k == "coop_frames") ctx->coop_frames = value != 0;
+        else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -1261,6 +1330,8 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "pdl") *value = g_pdl_user;
         else if (k == "multicast") *value = ctx->multicast;
         else if (k == "fold") *value = ctx->fold;
+        else if (k == "coop_frames") *value = ctx->coop_frames;
+        else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
@@ -1495,7 +1566,7 @@ int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, in
         // launch-level DAG (the read / write sets the concurrent issue uses), cost
         // model per launch kind in microseconds (measured C2 means):
         // ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
-        const double kc[7] = {2.5, 6.0, 9.0, 2.5, 2.8, 4.1, 2.0};
+        const double kc[8] = {2.5, 6.0, 9.0, 2.5, 2.8, 4.1, 2.0, 6.5};
         const std::size_t S = steps.size();
         std::vector<double> sfin(S, 0.0);
         double stot = 0, scrit = 0;
@@ -1521,6 +1592,36 @@ int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, in
             for (std::size_t j = 0; j < steps.size() && j < 400; ++j)
                 std::fprintf(stderr, "%zu lane %d kind %d waits %zu\n", j, d.lane[j], steps[j].kind,
                              d.waits[j].size());
+    });
+}
+
+// Diagnostics: the launch timeline of the last multiplication run with the
+// "trace" option (concurrent issue only).  Per launch: first CTA start and last
+// CTA end (us after the earliest start; -1 if the kernel has no hook), kind, lane, and up to
+// four launches on other lanes it waits for (-1 padded).  *n = launches.
+int wm_diag_trace(wm_ctx* ctx, int max, double* start_us, double* end_us, int* kind, int* lane,
+                  int* waits, int* n) {
+    return guard([&] {
+        const CachedPlan* cp = nullptr;
+        for (const auto& kv : ctx->cache)
+            if (kv.second.get() == ctx->traced) cp = kv.second.get();
+        if (!cp || !cp->dag) fail(E_INVALID, "no traced multiplication (set trace=1, dag>1)");
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        const int N = static_cast<int>(cp->steps.size());
+        *n = N;
+        std::vector<unsigned long long> t(2 * N);
+        WM_CUDA(cudaMemcpy(t.data(), cp->tl, t.size() * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (int j = 0; j < N; ++j) t0 = std::min(t0, t[2 * j]);
+        for (int j = 0; j < N && j < max; ++j) {
+            start_us[j] = t[2 * j] == ~0ull ? -1.0 : 1e-3 * static_cast<double>(t[2 * j] - t0);
+            end_us[j] = t[2 * j + 1] ? 1e-3 * static_cast<double>(t[2 * j + 1] - t0) : -1.0;
+            kind[j] = cp->steps[j].kind;
+            lane[j] = cp->dag->lane[j];
+            for (int w = 0; w < 4; ++w)
+                waits[4 * j + w] = w < static_cast<int>(cp->dag->waits[j].size()) ? cp->dag->waits[j][w] : -1;
+        }
     });
 }
 
