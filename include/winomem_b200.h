@@ -46,7 +46,8 @@ enum {
     WM_E_CONTRACT_VIOLATION = 11,/* contract_violation_error */
     WM_E_CUDA = 12,              /* device error (new) */
     WM_E_NCCL = 13,              /* communication error (new) */
-    WM_E_INVALID = 14            /* invalid argument / state (new) */
+    WM_E_INVALID = 14,           /* invalid argument / state (new) */
+    WM_E_UNKNOWN_SLOT = 15       /* unknown_slot_error */
 };
 
 enum { WM_FIELD_MODP = 0, WM_FIELD_REAL64 = 1 };
@@ -146,6 +147,24 @@ int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, i
                       wm_report* report);
 /* Per-schedule frame counts of the last plan on this thread: "name:count,..." */
 int wm_plan_schedule_calls(char* out, int len);
+
+/* Schedule DSL (schedule.hpp:261-684, executor.hpp:304-342).
+ * wm_run_parsed_schedule: run_parsed_schedule -- the schedule in `text` runs at
+ *   the top frame, its recursion tags dispatch to builtins.
+ * wm_parse_schedule: parse_schedule + render_schedule -- validates `text`
+ *   (WM_E_PARSE / WM_E_CONTRACT_VIOLATION), writes the canonical rendering to
+ *   out[len] (*needed = its length) and sets *builtin_match when the schedule
+ *   equals the builtin of the same name.
+ * wm_render_schedule: render_schedule of a builtin. */
+int wm_run_parsed_schedule(wm_ctx* ctx, const char* text, wm_dmat A, wm_dmat B, wm_dmat C,
+                           uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
+int wm_parse_schedule(const char* text, char* out, int len, int* needed, int* builtin_match);
+int wm_render_schedule(const char* name, char* out, int len, int* needed);
+/* run_parsed_schedule on host uint32 residues (the reference's Matrix&): like
+ * wm_run_variant_host_u32 with the schedule given as DSL text. */
+int wm_run_parsed_schedule_host_u32(wm_ctx* ctx, const char* text, uint64_t m, uint64_t k,
+                                    uint64_t n, uint32_t* A, uint32_t* B, uint32_t* C,
+                                    uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
 
 /* ---- boundary formats ------------------------------------------------------ */
 int wm_upload_u32(wm_ctx* ctx, wm_dmat dst, const uint32_t* host, uint64_t host_ld);

@@ -54,6 +54,9 @@ struct io_error : std::runtime_error {
 struct workspace_error : std::runtime_error {
     explicit workspace_error(const std::string& w) : std::runtime_error(w) {}
 };
+struct unknown_slot_error : std::runtime_error {
+    explicit unknown_slot_error(const std::string& w) : std::runtime_error(w) {}
+};
 struct unknown_schedule_error : std::runtime_error {
     explicit unknown_schedule_error(const std::string& w) : std::runtime_error(w) {}
 };
@@ -83,6 +86,7 @@ inline void check(int rc) {
         case WM_E_UNKNOWN_SCHEDULE: throw unknown_schedule_error(w);
         case WM_E_PARSE: throw parse_error(w);
         case WM_E_CONTRACT_VIOLATION: throw contract_violation_error(w);
+        case WM_E_UNKNOWN_SLOT: throw unknown_slot_error(w);
         default: throw device_error(w);
     }
 }
@@ -326,6 +330,52 @@ inline CostReport blocked_acc(Matrix& A, Matrix& B, Matrix& C, Elem alpha, Elem 
 // classical_mul (ring.hpp:315-384) on whole matrices
 inline void classical_mul(Matrix& C, Matrix& A, Matrix& B, Elem alpha, Elem beta) {
     run_variant("classic", A, B, C, {alpha, beta, 1});
+}
+
+// ---- schedule DSL (schedule.hpp:261-684, executor.hpp:304-342) -------------
+// A parsed schedule is carried as its validated text; the device planner
+// re-reads it (it is small) at each run.
+struct Schedule {
+    std::string name;
+    std::string text;       // canonical rendering (parses back to the same schedule)
+    bool builtin_match = false;
+};
+
+inline Schedule parse_schedule(const std::string& text) {
+    int need = 0, match = 0;
+    b200::check(wm_parse_schedule(text.c_str(), nullptr, 0, &need, &match));
+    std::string out(static_cast<std::size_t>(need) + 1, '\0');
+    b200::check(wm_parse_schedule(text.c_str(), &out[0], need + 1, &need, &match));
+    out.resize(static_cast<std::size_t>(need));
+    Schedule s;
+    s.text = out;
+    s.builtin_match = match != 0;
+    const auto sp = out.find(' '), nl = out.find('\n');
+    s.name = out.substr(sp + 1, nl - sp - 1);
+    return s;
+}
+
+inline std::string render_schedule(const Schedule& s) { return s.text; }
+
+inline Schedule builtin(const std::string& name) {
+    int need = 0;
+    b200::check(wm_render_schedule(name.c_str(), nullptr, 0, &need));
+    std::string out(static_cast<std::size_t>(need) + 1, '\0');
+    b200::check(wm_render_schedule(name.c_str(), &out[0], need + 1, &need));
+    out.resize(static_cast<std::size_t>(need));
+    return {name, out, true};
+}
+
+inline CostReport run_parsed_schedule(const Schedule& s, Matrix& A, Matrix& B, Matrix& C,
+                                      const MultiplyOptions& opt = {},
+                                      CostMeter* meter = nullptr) {
+    if (B.rows() != A.cols() || C.rows() != A.rows() || C.cols() != B.cols())
+        throw dimension_error("multiply dimensions do not conform");
+    wm_report r{};
+    b200::check(wm_run_parsed_schedule_host_u32(b200::context(A.mod().p()), s.text.c_str(),
+                                                A.rows(), A.cols(), B.cols(), A.data(), B.data(),
+                                                C.data(), opt.alpha, opt.beta, opt.cutoff, &r));
+    return b200::to_report(s.name, A.rows(), A.cols(), B.cols(), opt.cutoff, r, meter);
 }
 
 namespace models {

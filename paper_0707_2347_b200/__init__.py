@@ -11,6 +11,7 @@ from .winomem import (  # noqa: F401
     BUILTIN_NAMES, Context, CostReport, MatView, Matrix, Modulus, MultiplyOptions,
     alias_error, block_addsub, block_scale_copy, classical_mul, compare, contract_error,
     contract_violation_error, cuda_error, dimension_error, expected_costs, ipmm, ipovmm,
-    kDefaultModulus, multiply, odd_dimension_error, partial_overlap_error, plan_report,
-    quad_split, run_variant, run_variant_host, shape_error, unknown_schedule_error,
+    kDefaultModulus, multiply, odd_dimension_error, parse_error, parse_schedule,
+    partial_overlap_error, plan_report, quad_split, render_schedule, run_parsed_schedule,
+    run_variant, run_variant_host, shape_error, unknown_schedule_error, unknown_slot_error,
     variant_accumulates, workspace_error)

@@ -23,6 +23,8 @@ EXPORTS = [
     "wm_classical_mul", "wm_run_variant", "wm_ipmm", "wm_run_variant_real",
     "wm_run_variant_host_u32", "wm_plan_report", "wm_expected_costs", "wm_plan_schedule_calls",
     "wm_upload_u32", "wm_download_u32", "wm_fnv1a64_u32", "wm_fill_random",
+    "wm_run_parsed_schedule", "wm_parse_schedule", "wm_render_schedule",
+    "wm_run_parsed_schedule_host_u32",
 ]
 
 
@@ -80,6 +82,13 @@ def lib():
     L.wm_fnv1a64_u32.argtypes = [C.c_void_p, u64]
     L.wm_fnv1a64_u32.restype = u64
     L.wm_fill_random.argtypes = [ctx_p, wm_dmat, u64]
+    L.wm_run_parsed_schedule.argtypes = [ctx_p, C.c_char_p, wm_dmat, wm_dmat, wm_dmat, u32, u32,
+                                         i32, P(wm_report)]
+    L.wm_parse_schedule.argtypes = [C.c_char_p, C.c_char_p, i32, P(i32), P(i32)]
+    L.wm_render_schedule.argtypes = [C.c_char_p, C.c_char_p, i32, P(i32)]
+    L.wm_run_parsed_schedule_host_u32.argtypes = [ctx_p, C.c_char_p, u64, u64, u64, C.c_void_p,
+                                                  C.c_void_p, C.c_void_p, u32, u32, i32,
+                                                  P(wm_report)]
     _lib = L
     return L
 

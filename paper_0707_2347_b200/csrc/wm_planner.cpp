@@ -744,7 +744,17 @@ Plan plan_variant(const std::string& variant, Field f, std::uint64_t m, std::uin
     int t;
     std::string base;
 
-    if (variant == "ipmm") {
+    if (opt.parsed) {
+        // run_parsed_schedule (executor.hpp:304-342)
+        const Schedule& s = *opt.parsed;
+        if (s.square_only && !(m == k && k == n && is_pow2(n)))
+            fail(E_SHAPE, s.name + " requires square power-of-two dimensions");
+        ctx.policy = s.contract;
+        if (std::min({m, k, n}) <= static_cast<std::uint64_t>(cutoff))
+            classical_mul(ctx, C, A, B, alpha, beta);
+        else
+            run_schedule(s, A, B, C, alpha, beta, ctx);
+    } else if (variant == "ipmm") {
         // ipmm (drivers.hpp:137-158)
         if (B.cols != m || C.rows != m || C.cols != m || B.rows != k)
             fail(E_DIMENSION, "ipmm expects A n x k, B k x n, C n x n");

@@ -30,6 +30,9 @@ struct PlanOptions {
     // The FRAME kernels support leaf sizes that are multiples of this.
     int frame_align = 128;
     int frame_max_leaf = 1 << 20;
+    // run_parsed_schedule (executor.hpp:304-342): execute this schedule at the
+    // top frame instead of dispatching `variant` (recursion tags name builtins)
+    const Schedule* parsed = nullptr;
 };
 
 struct Plan {

@@ -738,6 +738,14 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         }
         return false;
     };
+    if (std::getenv("WM_PLAN_DUMP"))
+        for (std::size_t i = 0; i < plan.ops.size(); ++i) {
+            const Op& o = plan.ops[i];
+            std::fprintf(stderr, "op %zu kind %d %s/%d frame %d d=%d:%llu(%llux%llu)\n", i, o.kind,
+                         o.sched ? o.sched : "-", o.row, o.frame, o.d.region,
+                         static_cast<unsigned long long>(o.d.off), static_cast<unsigned long long>(o.d.rows),
+                         static_cast<unsigned long long>(o.d.cols));
+        }
     const bool fold = ctx.fold && !f.real;
     const std::vector<Fold> folds = fold ? plan_folds(plan) : std::vector<Fold>();
     std::vector<char> folded(plan.ops.size(), 0);
@@ -1081,13 +1089,15 @@ void check_dmat(const wm_dmat& m, const char* name) {
 }
 
 void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dmat& B,
-         const wm_dmat& C, Scalar alpha, Scalar beta, int cutoff, wm_report* rep) {
+         const wm_dmat& C, Scalar alpha, Scalar beta, int cutoff, wm_report* rep,
+         const Schedule* parsed = nullptr) {
     check_dmat(A, "A");
     check_dmat(B, "B");
     check_dmat(C, "C");
     if (B.rows != A.cols || C.rows != A.rows || C.cols != B.cols)
         fail(E_DIMENSION, "multiply dimensions do not conform");
     std::ostringstream key;
+    if (parsed) key << "dsl:" << render_schedule(*parsed);
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
@@ -1103,6 +1113,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     if (!cp) {
         PlanOptions opt;
         opt.fuse_frames = ctx->fuse_frames && frame_kernel_available();
+        opt.parsed = parsed;
         auto np = std::make_unique<CachedPlan>();
         np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld, alpha,
                                 beta, cutoff, opt);
@@ -1209,6 +1220,30 @@ void download(wm_ctx* ctx, std::uint32_t* host, std::uint64_t hld, const wm_dmat
                               ctx->stream));
     WM_CUDA(cudaMemcpy2DAsync(host, hld * 4, st, src.cols * 4, src.cols * 4, src.rows,
                               cudaMemcpyDeviceToHost, ctx->stream));
+}
+
+// Host u32 boundary (the reference's Matrix&): upload, run, download C and
+// whatever the contract lets the schedule overwrite.  C_in is uploaded whenever
+// the schedule reads it (beta != 0 or an accumulating schedule).
+void host_run(wm_ctx* ctx, const std::string& v, const Schedule* parsed, uint64_t m, uint64_t k,
+              uint64_t n, uint32_t* A, uint32_t* B, uint32_t* C, uint32_t alpha, uint32_t beta,
+              int cutoff, wm_report* report) {
+    if (ctx->f.real) fail(E_INVALID, "host u32 entry needs a MODP context");
+    if (!A || !B || !C) fail(E_INVALID, "null host buffer");
+    wm_dmat dA{ensure_buf(ctx, 0, m * k), m, k, k};
+    wm_dmat dB{ensure_buf(ctx, 1, k * n), k, n, n};
+    wm_dmat dC{ensure_buf(ctx, 2, m * n), m, n, n};
+    upload(ctx, dA, A, k);
+    upload(ctx, dB, B, n);
+    const bool acc = parsed ? parsed->accumulating : (v != "classic" && variant_accumulates(v));
+    if (beta % ctx->f.p != 0 || acc) upload(ctx, dC, C, n);
+    run(ctx, v, dA, dB, dC, modp_scalar(ctx->f, alpha), modp_scalar(ctx->f, beta), cutoff, report,
+        parsed);
+    download(ctx, C, n, dC);
+    const Contract c = parsed ? parsed->contract : variant_contract(v);
+    if (c == Contract::OverwriteA || c == Contract::OverwriteBoth) download(ctx, A, k, dA);
+    if (c == Contract::OverwriteB || c == Contract::OverwriteBoth) download(ctx, B, n, dB);
+    WM_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 template <class F>
@@ -1449,22 +1484,16 @@ int wm_run_variant_host_u32(wm_ctx* ctx, const char* variant, uint64_t m, uint64
                             uint32_t* A, uint32_t* B, uint32_t* C, uint32_t alpha, uint32_t beta,
                             int cutoff, wm_report* report) {
     return guard([&] {
-        if (ctx->f.real) fail(E_INVALID, "host u32 entry needs a MODP context");
-        if (!A || !B || !C) fail(E_INVALID, "null host buffer");
-        const std::string v = variant ? variant : "";
-        wm_dmat dA{ensure_buf(ctx, 0, m * k), m, k, k};
-        wm_dmat dB{ensure_buf(ctx, 1, k * n), k, n, n};
-        wm_dmat dC{ensure_buf(ctx, 2, m * n), m, n, n};
-        upload(ctx, dA, A, k);
-        upload(ctx, dB, B, n);
-        if (beta % ctx->f.p != 0) upload(ctx, dC, C, n);
-        run(ctx, v, dA, dB, dC, modp_scalar(ctx->f, alpha), modp_scalar(ctx->f, beta), cutoff,
-            report);
-        download(ctx, C, n, dC);
-        const Contract c = variant_contract(v);
-        if (c == Contract::OverwriteA || c == Contract::OverwriteBoth) download(ctx, A, k, dA);
-        if (c == Contract::OverwriteB || c == Contract::OverwriteBoth) download(ctx, B, n, dB);
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        host_run(ctx, variant ? variant : "", nullptr, m, k, n, A, B, C, alpha, beta, cutoff, report);
+    });
+}
+
+int wm_run_parsed_schedule_host_u32(wm_ctx* ctx, const char* text, uint64_t m, uint64_t k,
+                                    uint64_t n, uint32_t* A, uint32_t* B, uint32_t* C,
+                                    uint32_t alpha, uint32_t beta, int cutoff, wm_report* report) {
+    return guard([&] {
+        const Schedule s = parse_schedule(text ? text : "");
+        host_run(ctx, s.name, &s, m, k, n, A, B, C, alpha, beta, cutoff, report);
     });
 }
 
@@ -1637,6 +1666,49 @@ int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, i
             report->total_alloc_words = c.total;
             report->word_moves = c.moves;
         }
+    });
+}
+
+// run_parsed_schedule (executor.hpp:304-342): a schedule given as DSL text
+// executes at the top frame; its recursion tags dispatch to the builtins.
+int wm_run_parsed_schedule(wm_ctx* ctx, const char* text, wm_dmat A, wm_dmat B, wm_dmat C,
+                           uint32_t alpha, uint32_t beta, int cutoff, wm_report* report) {
+    return guard([&] {
+        if (ctx->f.real) fail(E_INVALID, "REAL64 context: parsed schedules run over Z/pZ");
+        const Schedule s = parse_schedule(text ? text : "");
+        run(ctx, s.name, A, B, C, modp_scalar(ctx->f, alpha), modp_scalar(ctx->f, beta), cutoff,
+            report, &s);
+    });
+}
+
+namespace {
+int put_text(const std::string& t, char* out, int len) {
+    if (out && len > 0) {
+        std::strncpy(out, t.c_str(), static_cast<std::size_t>(len) - 1);
+        out[len - 1] = 0;
+    }
+    return static_cast<int>(t.size());
+}
+}  // namespace
+
+// parse_schedule + render_schedule: validates DSL text (E_PARSE,
+// E_CONTRACT_VIOLATION) and writes this build's canonical rendering of it;
+// *builtin_match = 1 when it is instruction-for-instruction the builtin of the
+// same name.  Returns the status; *needed = rendered length.
+int wm_parse_schedule(const char* text, char* out, int len, int* needed, int* builtin_match) {
+    return guard([&] {
+        const Schedule s = parse_schedule(text ? text : "");
+        const int n = put_text(render_schedule(s), out, len);
+        if (needed) *needed = n;
+        if (builtin_match) *builtin_match = is_builtin(s.name) && same_schedule(s, builtin(s.name));
+    });
+}
+
+// render_schedule of a builtin (E_UNKNOWN_SCHEDULE otherwise).
+int wm_render_schedule(const char* name, char* out, int len, int* needed) {
+    return guard([&] {
+        const int n = put_text(render_schedule(builtin(name ? name : "")), out, len);
+        if (needed) *needed = n;
     });
 }
 

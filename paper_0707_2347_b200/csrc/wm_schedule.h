@@ -88,4 +88,11 @@ Schedule compile_program(const std::string& name, Contract c, bool accumulating,
                          bool square_only, const std::vector<TempDecl>& temps,
                          const char* program);
 
+// Schedule DSL (wm_dsl.cpp; the reference's text form, schedule.hpp:261-684):
+// parse_schedule throws E_PARSE / E_CONTRACT_VIOLATION; render_schedule emits
+// text that parses back to the same schedule (labels V1, V2, ...).
+Schedule parse_schedule(const std::string& text);
+std::string render_schedule(const Schedule& s);
+bool same_schedule(const Schedule& a, const Schedule& b);
+
 }  // namespace wm

@@ -36,6 +36,7 @@ enum Status : int {
     E_CUDA = 12,
     E_NCCL = 13,
     E_INVALID = 14,
+    E_UNKNOWN_SLOT = 15,  // unknown_slot_error (schedule.hpp:34-36)
 };
 
 struct Error : std::runtime_error {

@@ -72,6 +72,10 @@ class contract_violation_error(WinomemError):
     code = 11
 
 
+class unknown_slot_error(WinomemError):
+    code = 15
+
+
 class cuda_error(WinomemError):
     code = 12
 
@@ -88,7 +92,7 @@ _BY_CODE = {c.code: c for c in (dimension_error, odd_dimension_error, partial_ov
                                 alias_error, shape_error, contract_error, io_error,
                                 workspace_error, unknown_schedule_error, parse_error,
                                 contract_violation_error, cuda_error, nccl_error,
-                                invalid_argument)}
+                                invalid_argument, unknown_slot_error)}
 
 
 def _check(rc):
@@ -414,6 +418,45 @@ def run_variant(variant: str, A: Matrix, B: Matrix, C_: Matrix,
                                          opt.beta % p, opt.cutoff, C.byref(r)))
     ctx.leave()
     return _report(variant, A.rows(), A.cols(), B.cols(), opt.cutoff, r)
+
+
+def parse_schedule(text: str):
+    """parse_schedule (schedule.hpp:679-684): validate DSL text; returns
+    (canonical rendering, equals-the-builtin-of-that-name).  Raises parse_error /
+    contract_violation_error like the reference."""
+    L = _lib.lib()
+    need, match = C.c_int(), C.c_int()
+    _check(L.wm_parse_schedule(text.encode(), None, 0, C.byref(need), C.byref(match)))
+    buf = C.create_string_buffer(need.value + 1)
+    _check(L.wm_parse_schedule(text.encode(), buf, need.value + 1, C.byref(need), C.byref(match)))
+    return buf.value.decode(), bool(match.value)
+
+
+def render_schedule(name: str) -> str:
+    """render_schedule (schedule.hpp:617-684) of a builtin schedule."""
+    L = _lib.lib()
+    need = C.c_int()
+    _check(L.wm_render_schedule(name.encode(), None, 0, C.byref(need)))
+    buf = C.create_string_buffer(need.value + 1)
+    _check(L.wm_render_schedule(name.encode(), buf, need.value + 1, C.byref(need)))
+    return buf.value.decode()
+
+
+def run_parsed_schedule(text: str, A: Matrix, B: Matrix, C_: Matrix,
+                        opt: MultiplyOptions = None, **kw) -> CostReport:
+    """run_parsed_schedule (executor.hpp:304-342): the DSL schedule runs at the
+    top frame on the device; its recursion tags dispatch to the builtins."""
+    opt = opt or MultiplyOptions(**kw)
+    if A.real:
+        raise invalid_argument("parsed schedules run over Z/pZ")
+    ctx = _ctx_of(A, B, C_)
+    p = A.mod().p()
+    r = wm_report()
+    _check(_lib.lib().wm_run_parsed_schedule(ctx.h, text.encode(), A.view().dmat(),
+                                             B.view().dmat(), C_.view().dmat(), opt.alpha % p,
+                                             opt.beta % p, opt.cutoff, C.byref(r)))
+    ctx.leave()
+    return _report("parsed", A.rows(), A.cols(), B.cols(), opt.cutoff, r)
 
 
 def multiply(variant, A, B, C_, opt: MultiplyOptions = None, **kw) -> CostReport:

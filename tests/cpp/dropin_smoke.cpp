@@ -20,6 +20,17 @@ int main(int argc, char** argv) {
         return 4;
     } catch (const shape_error&) {
     }
+    // schedule DSL: every builtin renders and parses back to itself
+    for (const auto& name : builtin_names()) {
+        Schedule b = builtin(name);
+        Schedule t = parse_schedule(render_schedule(b));
+        if (!t.builtin_match || t.text != b.text || t.name != name) return 5;
+    }
+    try {
+        parse_schedule("1: S1 = A21 + NOPE @ X\n");
+        return 6;
+    } catch (const unknown_slot_error&) {
+    }
     if (plan_only_mode) {
         std::printf("plan-only ok\n");
         return 0;
@@ -38,11 +49,23 @@ int main(int argc, char** argv) {
                 for (std::size_t l = 0; l < 64; ++l) s += std::uint64_t(A.at(i, l)) * B.at(l, j) % 65521;
                 want.at(i, j) = static_cast<Elem>(s % 65521);
             }
+        Matrix C0 = C;
         CostMeter meter;
         run_variant(v, A, B, C, {1, acc ? 1u : 0u, 8}, &meter);
         if (!(C == want)) {
             std::printf("%s mismatch\n", v);
             return 10;
+        }
+        if (std::strcmp(v, "ipmm") != 0) {  // the same schedule as DSL text
+            Matrix A2(64, 64, mod), B2(64, 64, mod);
+            A2.fill_random(1);
+            B2.fill_random(2);
+            CostReport pr = run_parsed_schedule(parse_schedule(builtin(v).text), A2, B2, C0,
+                                                {1, acc ? 1u : 0u, 8});
+            if (!(C0 == want) || pr.mults != meter.mults || pr.peak_extra_words != meter.peak_extra_words) {
+                std::printf("%s parsed mismatch\n", v);
+                return 11;
+            }
         }
         std::printf("%s ok peak=%llu launches=%llu\n", v, (unsigned long long)meter.peak_extra_words,
                     (unsigned long long)meter.launches);

@@ -277,3 +277,45 @@ def test_partition_single_rank_gpu(W, O):
             assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (variant, n)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("v", ["std2", "acc3", "ip", "ovl", "ovl2", "ovr", "aclr", "accr",
+                               "acc2", "acr"])
+def test_run_parsed_schedule_reference_text(W, O, v):
+    """run_parsed_schedule (executor.hpp:304-342) on the reference's own DSL
+    rendering of each builtin: the parsed top frame runs on the device with the
+    same result (vs the oracle) and the same meter as run_variant."""
+    text = json.load(open(os.path.join(GOLD, "dsl_renderings.json")))["renderings"][v]
+    rect = v in ("std2", "acc3", "acr")
+    for (m, k, n, c) in ([(512, 256, 512, 64)] if rect else []) + [(1024, 1024, 1024, 128)]:
+        if v == "acr":
+            m, k, n = 1024, 512, 1024
+        acc = _acc(v)
+        al, be = (3, 7) if acc else (5, 0)
+        A, B, C = _problem(W, m, k, n, 7 + m + k, acc)
+        a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+        rep = W.run_parsed_schedule(text, A, B, C, alpha=al, beta=be, cutoff=c)
+        assert (C.to_u32() == O.classical_modp(a0, b0, c0 if acc else None, al, be)).all(), (v, m)
+        A2, B2, C2 = _problem(W, m, k, n, 7 + m + k, acc)
+        ref = W.run_variant(v, A2, B2, C2, alpha=al, beta=be, cutoff=c)
+        assert (rep.mults, rep.adds, rep.peak_extra_words) == (ref.mults, ref.adds,
+                                                               ref.peak_extra_words)
+
+
+def test_cpp_dropin_on_gpu():
+    """The C++ drop-in (include/winomem_b200.hpp) end to end on the device:
+    run_variant and run_parsed_schedule on host matrices vs a naive product."""
+    import subprocess
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = os.path.join(root, "tests", "cpp", "dropin_smoke.cpp")
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "dropin")
+        r = subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(root, "include"), src,
+                            "-o", exe, os.path.join(root, "paper_0707_2347_b200",
+                                                    "libwinomem_b200.so"),
+                            "-Wl,-rpath," + os.path.join(root, "paper_0707_2347_b200")],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
