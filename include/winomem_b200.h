@@ -160,6 +160,16 @@ int wm_run_parsed_schedule(wm_ctx* ctx, const char* text, wm_dmat A, wm_dmat B, 
                            uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
 int wm_parse_schedule(const char* text, char* out, int len, int* needed, int* builtin_match);
 int wm_render_schedule(const char* name, char* out, int len, int* needed);
+/* Matrix files (ring.hpp:386-449): text "rows cols p" + residues, or binary
+ * little-endian u64 (rows, cols, p) + u64 residues.  WM_E_IO on a bad header,
+ * a truncated body or a non-canonical entry (read_text / read_binary).
+ * *_device read into / write from a device matrix of the file's shape. */
+int wm_matrix_file_info(const char* path, int binary, uint64_t* rows, uint64_t* cols, uint32_t* p);
+int wm_matrix_read_host(const char* path, int binary, uint32_t* out, uint64_t capacity);
+int wm_matrix_write_host(const char* path, int binary, uint64_t rows, uint64_t cols, uint32_t p,
+                         const uint32_t* data);
+int wm_matrix_read_device(wm_ctx* ctx, const char* path, int binary, wm_dmat dst);
+int wm_matrix_write_device(wm_ctx* ctx, const char* path, int binary, wm_dmat src);
 /* run_parsed_schedule on host uint32 residues (the reference's Matrix&): like
  * wm_run_variant_host_u32 with the schedule given as DSL text. */
 int wm_run_parsed_schedule_host_u32(wm_ctx* ctx, const char* text, uint64_t m, uint64_t k,

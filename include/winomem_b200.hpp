@@ -18,6 +18,8 @@
 #include <memory>
 #include <mutex>
 #include <optional>
+#include <istream>
+#include <ostream>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -376,6 +378,67 @@ inline CostReport run_parsed_schedule(const Schedule& s, Matrix& A, Matrix& B, M
                                                 A.rows(), A.cols(), B.cols(), A.data(), B.data(),
                                                 C.data(), opt.alpha, opt.beta, opt.cutoff, &r));
     return b200::to_report(s.name, A.rows(), A.cols(), B.cols(), opt.cutoff, r, meter);
+}
+
+// ---- matrix file formats (ring.hpp:386-449), on the host Matrix --------------
+// Text: "rows cols p" then rows*cols residues; binary: little-endian u64
+// (rows, cols, p) then u64 residues.  io_error on a bad header, truncation or
+// a non-canonical entry.  (wm_matrix_read_device / _write_device move files
+// straight to and from device matrices.)
+inline void write_text(const Matrix& a, std::ostream& os) {
+    os << a.rows() << ' ' << a.cols() << ' ' << a.mod().p() << '\n';
+    for (std::size_t i = 0; i < a.rows(); ++i) {
+        for (std::size_t j = 0; j < a.cols(); ++j) os << (j ? " " : "") << a.at(i, j);
+        os << '\n';
+    }
+}
+
+inline Matrix read_text(std::istream& is) {
+    std::uint64_t r, c, p;
+    if (!(is >> r >> c >> p)) throw io_error("bad matrix text header");
+    Matrix a(r, c, Modulus(static_cast<std::uint32_t>(p)));
+    for (std::size_t i = 0; i < r; ++i)
+        for (std::size_t j = 0; j < c; ++j) {
+            std::uint64_t v;
+            if (!(is >> v)) throw io_error("matrix text truncated");
+            if (v >= p) throw io_error("matrix entry not a canonical residue");
+            a.at(i, j) = static_cast<Elem>(v);
+        }
+    return a;
+}
+
+namespace b200 {
+inline void put_le(std::ostream& os, std::uint64_t v) {
+    char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<char>(v >> (8 * i));
+    os.write(b, 8);
+}
+inline std::uint64_t get_le(std::istream& is) {
+    unsigned char b[8];
+    is.read(reinterpret_cast<char*>(b), 8);
+    if (!is) throw io_error("matrix binary truncated");
+    std::uint64_t v = 0;
+    for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(b[i]) << (8 * i);
+    return v;
+}
+}  // namespace b200
+
+inline void write_binary(const Matrix& a, std::ostream& os) {
+    b200::put_le(os, a.rows());
+    b200::put_le(os, a.cols());
+    b200::put_le(os, a.mod().p());
+    for (std::size_t i = 0; i < a.rows() * a.cols(); ++i) b200::put_le(os, a.data()[i]);
+}
+
+inline Matrix read_binary(std::istream& is) {
+    const std::uint64_t r = b200::get_le(is), c = b200::get_le(is), p = b200::get_le(is);
+    Matrix a(r, c, Modulus(static_cast<std::uint32_t>(p)));
+    for (std::size_t i = 0; i < r * c; ++i) {
+        const std::uint64_t v = b200::get_le(is);
+        if (v >= p) throw io_error("matrix entry not a canonical residue");
+        a.data()[i] = static_cast<Elem>(v);
+    }
+    return a;
 }
 
 namespace models {

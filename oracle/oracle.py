@@ -80,6 +80,10 @@ def ref():
         R.ref_hash.argtypes = [P_u32, u64]
         R.ref_hash.restype = u64
         R.ref_render_builtin.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        R.ref_write_matrix.argtypes = [C.c_char_p, C.c_int, u64, u64, u32, C.c_void_p]
+        R.ref_read_matrix.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.c_void_p,
+                                      u64]
         _REF = R
     return _REF
 
@@ -183,3 +187,26 @@ def ref_render_builtin(name):
     if n < 0:
         raise RefError(-n, name)
     return buf.value.decode()
+
+
+def ref_write_matrix(path, a, p=DEFAULT_P, binary=False):
+    """The reference's write_text / write_binary (ring.hpp:390-434)."""
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    rc = ref().ref_write_matrix(path.encode(), 1 if binary else 0, a.shape[0], a.shape[1], p,
+                                a.ctypes.data)
+    if rc < 0:
+        raise RefError(-rc, path)
+
+
+def ref_read_matrix(path, binary=False):
+    """The reference's read_text / read_binary (ring.hpp:401-446) -> (array, p);
+    raises RefError(code) on a reference exception."""
+    r, c, p = C.c_uint64(), C.c_uint64(), C.c_uint32()
+    rc = ref().ref_read_matrix(path.encode(), 1 if binary else 0, C.byref(r), C.byref(c),
+                               C.byref(p), None, 0)
+    if rc < 0:
+        raise RefError(-rc, path)
+    out = np.zeros((r.value, c.value), dtype=np.uint32)
+    ref().ref_read_matrix(path.encode(), 1 if binary else 0, C.byref(r), C.byref(c), C.byref(p),
+                          out.ctypes.data, out.size)
+    return out, p.value

@@ -14,6 +14,8 @@
 //   ref_block_addsub     -> winomem::block_addsub  (inc/ring.hpp:241-278)
 //   ref_fill_random      -> Matrix::fill_random    (inc/ring.hpp:202-205)
 //   ref_hash             -> fnv1a64                (inc/ring.hpp:107-114)
+#include <fstream>
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -159,6 +161,37 @@ int ref_render_builtin(const char* name, char* out, int len) {
         std::string s = render_schedule(builtin(name));
         put_err(out, len, s.c_str());
         return static_cast<int>(s.size());
+    } catch (const std::exception& e) {
+        return -code_of(e);
+    }
+}
+
+// Matrix file formats (ring.hpp:386-449): write a matrix with the reference's
+// writers / read one back with its readers (status < 0: exception code).
+int ref_write_matrix(const char* path, int binary, std::uint64_t rows, std::uint64_t cols,
+                     std::uint32_t p, const std::uint32_t* data) {
+    try {
+        Matrix a(rows, cols, Modulus(p));
+        std::copy(data, data + rows * cols, a.data());
+        std::ofstream os(path, binary ? std::ios::binary : std::ios::out);
+        if (binary) write_binary(a, os);
+        else write_text(a, os);
+        return 0;
+    } catch (const std::exception& e) {
+        return -code_of(e);
+    }
+}
+
+int ref_read_matrix(const char* path, int binary, std::uint64_t* rows, std::uint64_t* cols,
+                    std::uint32_t* p, std::uint32_t* out, std::uint64_t cap) {
+    try {
+        std::ifstream is(path, binary ? std::ios::binary : std::ios::in);
+        Matrix a = binary ? read_binary(is) : read_text(is);
+        *rows = a.rows();
+        *cols = a.cols();
+        *p = a.mod().p();
+        if (out && a.size() <= cap) std::copy(a.data(), a.data() + a.size(), out);
+        return 0;
     } catch (const std::exception& e) {
         return -code_of(e);
     }

@@ -23,6 +23,7 @@
 #include "../../include/winomem_b200.h"
 #include "wm_device.h"
 #include "wm_frame.h"
+#include "wm_io.h"
 #include "wm_fused.h"
 #include "wm_gemm.h"
 #include "wm_launch.h"
@@ -1709,6 +1710,52 @@ int wm_render_schedule(const char* name, char* out, int len, int* needed) {
     return guard([&] {
         const int n = put_text(render_schedule(builtin(name ? name : "")), out, len);
         if (needed) *needed = n;
+    });
+}
+
+// ---- matrix files (ring.hpp:386-449) ---------------------------------------
+int wm_matrix_file_info(const char* path, int binary, uint64_t* rows, uint64_t* cols, uint32_t* p) {
+    return guard([&] {
+        const MatrixFile m = read_matrix_file(path ? path : "", binary != 0, true);
+        *rows = m.rows;
+        *cols = m.cols;
+        *p = m.p;
+    });
+}
+
+int wm_matrix_read_host(const char* path, int binary, uint32_t* out, uint64_t capacity) {
+    return guard([&] {
+        const MatrixFile m = read_matrix_file(path ? path : "", binary != 0);
+        if (m.data.size() > capacity) fail(E_INVALID, "output buffer smaller than the matrix");
+        std::memcpy(out, m.data.data(), m.data.size() * sizeof(uint32_t));
+    });
+}
+
+int wm_matrix_write_host(const char* path, int binary, uint64_t rows, uint64_t cols, uint32_t p,
+                         const uint32_t* data) {
+    return guard([&] { write_matrix_file(path ? path : "", binary != 0, rows, cols, p, data); });
+}
+
+// read straight into a device matrix (residues converted on the device); the
+// file's shape must equal dst's and its modulus the context's
+int wm_matrix_read_device(wm_ctx* ctx, const char* path, int binary, wm_dmat dst) {
+    return guard([&] {
+        if (ctx->f.real) fail(E_INVALID, "matrix files hold residues: MODP context needed");
+        const MatrixFile m = read_matrix_file(path ? path : "", binary != 0);
+        if (m.rows != dst.rows || m.cols != dst.cols) fail(E_DIMENSION, "file shape differs from the matrix");
+        if (m.p != ctx->f.p) fail(E_DIMENSION, "file modulus differs from the context's");
+        upload(ctx, dst, m.data.data(), m.cols);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int wm_matrix_write_device(wm_ctx* ctx, const char* path, int binary, wm_dmat src) {
+    return guard([&] {
+        if (ctx->f.real) fail(E_INVALID, "matrix files hold residues: MODP context needed");
+        std::vector<uint32_t> h(src.rows * src.cols);
+        download(ctx, h.data(), src.cols, src);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        write_matrix_file(path ? path : "", binary != 0, src.rows, src.cols, ctx->f.p, h.data());
     });
 }
 

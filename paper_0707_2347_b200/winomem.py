@@ -420,6 +420,59 @@ def run_variant(variant: str, A: Matrix, B: Matrix, C_: Matrix,
     return _report(variant, A.rows(), A.cols(), B.cols(), opt.cutoff, r)
 
 
+# ---- matrix files (ring.hpp:386-449) -----------------------------------------
+def matrix_file_info(path: str, binary=False):
+    """(rows, cols, p) from a matrix file header (io_error if malformed)."""
+    r, c, p = C.c_uint64(), C.c_uint64(), C.c_uint32()
+    _check(_lib.lib().wm_matrix_file_info(path.encode(), 1 if binary else 0, C.byref(r),
+                                          C.byref(c), C.byref(p)))
+    return r.value, c.value, p.value
+
+
+def read_matrix_host(path: str, binary=False):
+    """read_text / read_binary into a host u32 array -> (array, p)."""
+    r, c, p = matrix_file_info(path, binary)
+    out = np.empty((r, c), dtype=np.uint32)
+    _check(_lib.lib().wm_matrix_read_host(path.encode(), 1 if binary else 0, out.ctypes.data,
+                                          out.size))
+    return out, p
+
+
+def write_matrix_host(path: str, a: np.ndarray, p=kDefaultModulus, binary=False):
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    _check(_lib.lib().wm_matrix_write_host(path.encode(), 1 if binary else 0, a.shape[0],
+                                           a.shape[1], p, a.ctypes.data))
+
+
+def read_text(path: str, device=0, binary=False) -> "Matrix":
+    """read_text (ring.hpp:401-412): a device Matrix straight from the file."""
+    r, c, p = matrix_file_info(path, binary)
+    M = Matrix(r, c, Modulus(p), device=device)
+    ctx = M.ctx()
+    ctx.enter()
+    _check(_lib.lib().wm_matrix_read_device(ctx.h, path.encode(), 1 if binary else 0,
+                                            M.view().dmat()))
+    return M
+
+
+def read_binary(path: str, device=0) -> "Matrix":
+    """read_binary (ring.hpp:436-446)."""
+    return read_text(path, device, binary=True)
+
+
+def write_text(M: "Matrix", path: str, binary=False):
+    """write_text (ring.hpp:390-399) from a device Matrix."""
+    ctx = M.ctx()
+    ctx.enter()
+    _check(_lib.lib().wm_matrix_write_device(ctx.h, path.encode(), 1 if binary else 0,
+                                             M.view().dmat()))
+
+
+def write_binary(M: "Matrix", path: str):
+    """write_binary (ring.hpp:428-434)."""
+    write_text(M, path, binary=True)
+
+
 def parse_schedule(text: str):
     """parse_schedule (schedule.hpp:679-684): validate DSL text; returns
     (canonical rendering, equals-the-builtin-of-that-name).  Raises parse_error /

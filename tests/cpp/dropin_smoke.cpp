@@ -3,6 +3,7 @@
 // checks C against a naive product.
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 
 #include "winomem_b200.hpp"
 
@@ -30,6 +31,21 @@ int main(int argc, char** argv) {
         parse_schedule("1: S1 = A21 + NOPE @ X\n");
         return 6;
     } catch (const unknown_slot_error&) {
+    }
+    {  // matrix file formats round trip (ring.hpp:386-449)
+        Modulus m7(101);
+        Matrix a(3, 4, m7);
+        a.fill_random(9);
+        std::stringstream t, b;
+        write_text(a, t);
+        write_binary(a, b);
+        if (!(read_text(t) == a) || !(read_binary(b) == a)) return 7;
+        std::stringstream bad("2 2 7\n1 2 3 9\n");
+        try {
+            read_text(bad);
+            return 8;
+        } catch (const io_error&) {
+        }
     }
     if (plan_only_mode) {
         std::printf("plan-only ok\n");
