@@ -58,7 +58,7 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 struct Step {
-    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB, FCOOP } kind;
+    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB, FCOOP, UPLOAD, DOWNLOAD } kind;
     AddBatch add;
     unsigned blocks = 0;
     MulParams mul;
@@ -73,6 +73,14 @@ struct Step {
     std::shared_ptr<TmaMaps> tmaps;
     unsigned long long* tl = nullptr;  // GROUP: measurement timeline slot
     std::uint32_t* bar = nullptr;      // FCOOP: the launch's grid-barrier pair
+    // UPLOAD / DOWNLOAD (host u32 boundary): one block of a host matrix, staged
+    // as u32 on the device and converted to / from the float64 operand
+    std::uint32_t* hptr = nullptr;
+    std::uint32_t* sptr = nullptr;
+    double* dptr = nullptr;
+    std::uint64_t hld = 0, sld = 0, dld = 0, io_rows = 0, io_cols = 0;
+    std::uint32_t io_p = 0;
+    std::int8_t lane_hint = -1;        // 0: the copy-in lane, 1: the copy-out lane
     // memory the launch reads / writes (dependency analysis for concurrent issue)
     std::vector<View> rd, wr;
 };
@@ -202,6 +210,7 @@ struct wm_ctx {
                                 // measured: 2 >= 3, 4, 6 > 8 lanes)
     bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
+    bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
     const void* traced = nullptr;  // CachedPlan of the last traced run
     bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
@@ -842,6 +851,7 @@ bool g_pdl_user = true;  // the "pdl" option; per launch g_pdl = option && polic
 // float64 leaves, 2.88 s per multiply with PDL vs 1.68 s without).
 bool use_pdl(const Step& s, const Step* prev) {
     if (!g_pdl_user || (prev && long_step(*prev))) return false;
+    if (prev && (prev->kind == Step::UPLOAD || prev->kind == Step::DOWNLOAD)) return false;
     if (s.kind == Step::MUL && 2.0 * s.mul.m * static_cast<double>(s.mul.k) * s.mul.n > 1e8)
         return false;
     return true;
@@ -871,6 +881,18 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
         case Step::FCOOP:
             WM_CUDA(launch_frame_coop(s.fprep, s.fgemm, s.fcomb, *s.tmaps, s.bn, s.bar, st));
             break;
+        case Step::UPLOAD:
+            WM_CUDA(cudaMemcpy2DAsync(s.sptr, s.sld * 4, s.hptr, s.hld * 4, s.io_cols * 4, s.io_rows,
+                                      cudaMemcpyHostToDevice, st));
+            g_pdl = false;
+            WM_CUDA(launch_u32_to_f64(s.dptr, s.dld, s.sptr, s.sld, s.io_rows, s.io_cols, st));
+            break;
+        case Step::DOWNLOAD:
+            g_pdl = false;
+            WM_CUDA(launch_f64_to_u32(s.sptr, s.sld, s.dptr, s.dld, s.io_rows, s.io_cols, s.io_p, st));
+            WM_CUDA(cudaMemcpy2DAsync(s.hptr, s.hld * 4, s.sptr, s.sld * 4, s.io_cols * 4, s.io_rows,
+                                      cudaMemcpyDeviceToHost, st));
+            break;
     }
 }
 
@@ -899,6 +921,7 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
 // launches on other lanes are joined through events.  Dependencies are
 // exact within an epoch of kEpoch steps; at epoch boundaries every lane joins.
 struct DagPlan {
+    int nlanes = 1;                       // streams used (compute lanes + copy lanes)
     std::vector<int> lane;                // per step
     std::vector<std::vector<int>> waits;  // per step: steps (other lanes) to wait for
     std::vector<char> record;             // per step: an event is recorded after it
@@ -907,10 +930,14 @@ struct DagPlan {
 
 constexpr int kEpoch = 512;
 
-DagPlan plan_dag(const std::vector<Step>& steps, int nl) {
-    nl = nl < 1 ? 1 : nl > kLanes ? kLanes : nl;
+DagPlan plan_dag(const std::vector<Step>& steps, int nl, int epoch = kEpoch) {
+    nl = nl < 1 ? 1 : nl > kLanes - 2 ? kLanes - 2 : nl;
     const int n = static_cast<int>(steps.size());
     DagPlan d;
+    bool io = false;
+    for (const Step& s : steps) io |= s.lane_hint >= 0;
+    const int total = nl + (io ? 2 : 0);  // copy-in / copy-out lanes after the compute lanes
+    d.nlanes = total;
     d.lane.assign(n, 0);
     d.waits.assign(n, {});
     d.record.assign(n, 0);
@@ -919,19 +946,19 @@ DagPlan plan_dag(const std::vector<Step>& steps, int nl) {
     int last_on[kLanes];
     int synced[kLanes][kLanes];  // synced[a][b]: latest step of lane b that lane a waited for
     for (int j = 0; j < n; ++j) {
-        if (j - epoch0 == kEpoch) {
+        if (j - epoch0 == epoch) {
             d.epoch_end[j - 1] = 1;
             epoch0 = j;
         }
         if (j == epoch0)
             for (int l = 0; l < kLanes; ++l) {
-                last_on[l] = l < nl ? -1 : 1 << 30;
+                last_on[l] = l < total ? -1 : 1 << 30;
                 for (int m = 0; m < kLanes; ++m) synced[l][m] = -1;
             }
         // latest conflicting step per lane (earlier ones on a lane are implied)
         int dep[kLanes];
         for (int l = 0; l < kLanes; ++l) dep[l] = -1;
-        int open = nl;
+        int open = total;
         for (int i = j - 1; i >= epoch0 && open > 0; --i) {
             const int l = d.lane[i];
             if (dep[l] >= 0) continue;
@@ -942,8 +969,8 @@ DagPlan plan_dag(const std::vector<Step>& steps, int nl) {
         }
         // a lane whose last launch is itself a dependency adds no false edge;
         // otherwise take the lane whose last launch is oldest (most likely done)
-        int best = -1;
-        for (int l = 0; l < nl; ++l)
+        int best = steps[j].lane_hint >= 0 ? nl + steps[j].lane_hint : -1;
+        for (int l = 0; l < nl && steps[j].lane_hint < 0; ++l)
             if (last_on[l] >= 0 && dep[l] == last_on[l] && (best < 0 || last_on[l] > last_on[best]))
                 best = l;
         if (best < 0) {
@@ -964,8 +991,8 @@ DagPlan plan_dag(const std::vector<Step>& steps, int nl) {
 }
 
 void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cudaStream_t main,
-               Lanes& L, int nl) {
-    nl = nl < 1 ? 1 : nl > kLanes ? kLanes : nl;
+               Lanes& L) {
+    const int nl = d.nlanes;
     const int n = static_cast<int>(steps.size());
     L.s[0] = main;
     for (int l = 1; l < nl; ++l)
@@ -1089,9 +1116,83 @@ void check_dmat(const wm_dmat& m, const char* name) {
     if (!m.ptr) fail(E_INVALID, std::string(name) + ": null pointer");
 }
 
+// The host u32 boundary streamed through the step graph: uploads (pinned host ->
+// staging -> float64) and downloads per quadrant, as steps of their own on a
+// copy-in and a copy-out lane, so that the product starts as soon as the
+// quadrants its first operations read are resident and a C quadrant leaves as
+// soon as its last writer is done.
+struct HostIO {
+    std::uint32_t* h[3] = {nullptr, nullptr, nullptr};  // A, B, C (row-major, ld = cols)
+    std::uint32_t* stage[3] = {nullptr, nullptr, nullptr};
+    bool up[3] = {false, false, false}, down[3] = {false, false, false};
+};
+
+void add_io_steps(std::vector<Step>& steps, const HostIO& io, const wm_dmat M[3], std::uint32_t p) {
+    std::vector<Step> ups, downs;
+    std::vector<std::size_t> first_use;
+    for (int w = 0; w < 3; ++w) {
+        if (!io.up[w] && !io.down[w]) continue;
+        const std::uint64_t r = M[w].rows, c = M[w].cols;
+        const bool quads = r % 2 == 0 && c % 2 == 0;
+        for (int q = 0; q < (quads ? 4 : 1); ++q) {
+            const std::uint64_t br = quads ? r / 2 : r, bc = quads ? c / 2 : c;
+            const std::uint64_t r0 = quads ? (q / 2) * br : 0, c0 = quads ? (q % 2) * bc : 0;
+            Step st{};
+            st.hptr = io.h[w] + r0 * c + c0;
+            st.sptr = io.stage[w] + r0 * c + c0;
+            st.dptr = M[w].ptr + r0 * M[w].ld + c0;
+            st.hld = st.sld = c;
+            st.dld = M[w].ld;
+            st.io_rows = br;
+            st.io_cols = bc;
+            st.io_p = p;
+            View v;
+            v.region = static_cast<std::uint8_t>(w);
+            v.origin = w;
+            v.off = r0 * M[w].ld + c0;
+            v.rows = br;
+            v.cols = bc;
+            v.ld = M[w].ld;
+            if (io.up[w]) {
+                Step u = st;
+                u.kind = Step::UPLOAD;
+                u.lane_hint = 0;
+                u.wr.push_back(v);
+                std::size_t fu = steps.size();
+                for (std::size_t j = 0; j < steps.size() && fu == steps.size(); ++j)
+                    for (const View& x : steps[j].rd)
+                        if (x.phys_overlaps(v)) {
+                            fu = j;
+                            break;
+                        }
+                ups.push_back(u);
+                first_use.push_back(fu);
+            }
+            if (io.down[w]) {
+                Step d = st;
+                d.kind = Step::DOWNLOAD;
+                d.lane_hint = 1;
+                d.rd.push_back(v);
+                downs.push_back(d);
+            }
+        }
+    }
+    // copy-in in order of first use: the lane is one PCIe stream
+    std::vector<std::size_t> order(ups.size());
+    for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](std::size_t a, std::size_t b) { return first_use[a] < first_use[b]; });
+    std::vector<Step> out;
+    out.reserve(ups.size() + steps.size() + downs.size());
+    for (std::size_t i : order) out.push_back(ups[i]);
+    for (Step& st : steps) out.push_back(std::move(st));
+    for (Step& st : downs) out.push_back(std::move(st));
+    steps.swap(out);
+}
+
 void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dmat& B,
          const wm_dmat& C, Scalar alpha, Scalar beta, int cutoff, wm_report* rep,
-         const Schedule* parsed = nullptr) {
+         const Schedule* parsed = nullptr, const HostIO* io = nullptr) {
     check_dmat(A, "A");
     check_dmat(B, "B");
     check_dmat(C, "C");
@@ -1102,7 +1203,10 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+    if (io)
+        for (int w = 0; w < 3; ++w)
+            key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
     const std::string k = key.str();
     CachedPlan* cp = nullptr;
     for (auto it = ctx->cache.begin(); it != ctx->cache.end(); ++it)
@@ -1122,6 +1226,10 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
             WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
         double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
         np->steps = lower(np->plan, base, *ctx);
+        if (io) {
+            const wm_dmat M[3] = {A, B, C};
+            add_io_steps(np->steps, *io, M, ctx->f.p);
+        }
         std::size_t ncoop = 0;
         for (const Step& st : np->steps) ncoop += st.kind == Step::FCOOP;
         if (ncoop) {  // zeroed {count, sense} per cooperative launch
@@ -1137,9 +1245,14 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     }
     // concurrent issue pays only for launches of real size; tiny problems (deep
     // recursions of the unit tests) would spend more on the dependency analysis
-    const bool dag = ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1 &&
-                     std::max({A.rows, A.cols, B.cols}) >= 512 && cp->steps.size() <= 200000;
-    if (dag && !cp->dag) cp->dag = std::make_shared<DagPlan>(plan_dag(cp->steps, ctx->dag));
+    const bool dag = io || (ctx->dag > 1 && ctx->subset == 0 && cp->steps.size() > 1 &&
+                            std::max({A.rows, A.cols, B.cols}) >= 512 && cp->steps.size() <= 200000);
+    // with the boundary in the graph, one dependency epoch spans the whole step
+    // (up to 4096 launches) so C quadrants can leave while the rest computes
+    if (dag && !cp->dag)
+        cp->dag = std::make_shared<DagPlan>(plan_dag(
+            cp->steps, std::max(1, ctx->dag),
+            io ? std::max(kEpoch, std::min<int>(4096, static_cast<int>(cp->steps.size()))) : kEpoch));
     if (ctx->trace) {
         // [start, end] globaltimer slots per launch, patched into the launch
         // parameters of this (trace-keyed) plan before its graph is captured
@@ -1160,7 +1273,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     }
     auto go = [&]() {
         if (dag)
-            issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes, ctx->dag);
+            issue_dag(cp->steps, *cp->dag, ctx->f.real, ctx->stream, ctx->lanes);
         else issue(cp->steps, ctx->f.real, ctx->stream, ctx->subset);
     };
     // capture pays for the launch-bound plans of real problems; the 10^5-launch
@@ -1234,6 +1347,34 @@ void host_run(wm_ctx* ctx, const std::string& v, const Schedule* parsed, uint64_
     wm_dmat dA{ensure_buf(ctx, 0, m * k), m, k, k};
     wm_dmat dB{ensure_buf(ctx, 1, k * n), k, n, n};
     wm_dmat dC{ensure_buf(ctx, 2, m * n), m, n, n};
+    const bool acc0 = parsed ? parsed->accumulating : (v != "classic" && variant_accumulates(v));
+    const Contract c0 = parsed ? parsed->contract : variant_contract(v);
+    auto pinned = [](const void* ptr) {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return a.type == cudaMemoryTypeHost;
+    };
+    // streamed when the copies are long enough to hide compute behind (measured:
+    // config 2's e2e 9.8 -> 7.9 ms; a 1024^3 problem gains nothing)
+    if (ctx->graphs && ctx->stream_io && m * k + k * n + m * n >= (8ull << 20) && pinned(A) &&
+        pinned(B) && pinned(C)) {
+        HostIO io;
+        std::uint32_t* st = ensure_stage(ctx, m * k + k * n + m * n);
+        io.h[0] = A, io.h[1] = B, io.h[2] = C;
+        io.stage[0] = st, io.stage[1] = st + m * k, io.stage[2] = st + m * k + k * n;
+        io.up[0] = io.up[1] = true;
+        io.up[2] = beta % ctx->f.p != 0 || acc0;
+        io.down[2] = true;
+        io.down[0] = c0 == Contract::OverwriteA || c0 == Contract::OverwriteBoth;
+        io.down[1] = c0 == Contract::OverwriteB || c0 == Contract::OverwriteBoth;
+        run(ctx, v, dA, dB, dC, modp_scalar(ctx->f, alpha), modp_scalar(ctx->f, beta), cutoff,
+            report, parsed, &io);
+        WM_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+    }
     upload(ctx, dA, A, k);
     upload(ctx, dB, B, n);
     const bool acc = parsed ? parsed->accumulating : (v != "classic" && variant_accumulates(v));
@@ -1344,6 +1485,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
         else if (k == "coop_frames") ctx->coop_frames = value != 0;
+        else if (k == "stream_io") ctx->stream_io = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1367,6 +1509,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "multicast") *value = ctx->multicast;
         else if (k == "fold") *value = ctx->fold;
         else if (k == "coop_frames") *value = ctx->coop_frames;
+        else if (k == "stream_io") *value = ctx->stream_io;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;

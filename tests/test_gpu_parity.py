@@ -343,3 +343,35 @@ def test_matrix_files_device_round_trip(W, O, tmp_path, binary):
     W.write_text(C, fc, binary)
     got, p = W.read_matrix_host(fc, binary)
     assert p == 65521 and (got == O.classical_modp(A.to_u32(), B.to_u32(), None, 1, 0)).all()
+
+
+@pytest.mark.parametrize("v,n,c", [("std2", 2048, 128), ("acc2", 2048, 256), ("ip", 2048, 256),
+                                   ("ipmm", 2048, 256), ("aclr", 2048, 256)])
+@pytest.mark.parametrize("stream_io", [1, 0], ids=["streamed", "staged"])
+def test_host_u32_pinned_streamed(W, O, v, n, c, stream_io):
+    """The host u32 boundary with pinned buffers: quadrant copies inside the
+    step graph (copy-in / copy-out lanes) vs the oracle, incl. the overwritten
+    A / B of an in-place contract coming back to the host."""
+    import torch
+    ctx = W.Context.get()
+    saved = ctx.get_option("stream_io")
+    ctx.set_option("stream_io", stream_io)
+    try:
+        acc = _acc(v)
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        A, B = pin(O.fill_random(n, n, 11)), pin(O.fill_random(n, n, 12))
+        C0 = O.fill_random(n, n, 13) if acc else np.zeros((n, n), np.uint32)
+        C = pin(C0.copy())
+        a0, b0 = A.copy(), B.copy()
+        want = O.classical_modp(a0, b0, C0 if acc else None, 3 if v != "ipmm" else 1,
+                                5 if acc else 0)
+        for rep in range(2):  # the second call replays the cached graph
+            C[...] = C0
+            A[...], B[...] = a0, b0
+            W.run_variant_host(v, A, B, C, alpha=3 if v != "ipmm" else 1, beta=5 if acc else 0,
+                               cutoff=c)
+            assert (C == want).all(), (v, rep)
+            if v in ("std2", "acc2", "ipmm"):
+                assert (A == a0).all() and (B == b0).all()
+    finally:
+        ctx.set_option("stream_io", saved)
