@@ -502,12 +502,14 @@ def run_partitioned(args, cfg, rank, world, local):
     import torch.distributed as dist
 
     import paper_0707_2347_b200 as W
-    from paper_0707_2347_b200.dist import (CudaBackend, local_variant, makespan_bound,
-                                           partitioned_multiply)
+    from paper_0707_2347_b200.dist import (CudaBackend, choose_levels, local_variant,
+                                           makespan_bound, partitioned_multiply)
 
     real = cfg["field"] == "real"
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
-    lv = local_variant(cfg["variant"], m // 2, k // 2, n // 2)
+    levels = choose_levels(world)
+    f = 2 ** levels
+    lv = local_variant(cfg["variant"], m // f, k // f, n // f)
     be = CudaBackend(65521, lv, cfg["cutoff"], local, real=real)
     dev = f"cuda:{local}"
     A = B = C = None
@@ -522,7 +524,7 @@ def run_partitioned(args, cfg, rank, world, local):
     ctxs = W.Context.get(local, 65521, real)
 
     def step():
-        partitioned_multiply(A, B, C, cfg["alpha"], cfg["beta"], be)
+        partitioned_multiply(A, B, C, cfg["alpha"], cfg["beta"], be, levels=levels)
 
     parity = None
     step()
@@ -560,9 +562,9 @@ def run_partitioned(args, cfg, rank, world, local):
                                                                    cfg["seed"] + 2),
             "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
                        "m": m, "k": k, "n": n, "cutoff": cfg["cutoff"],
-                       "parallelism": f"7-way top-level product partition over {world} GPUs "
-                                      f"(NCCL p2p), local schedule {lv}",
-                       "makespan_bound": makespan_bound(world)},
+                       "parallelism": f"{7 ** levels}-way product partition ({levels} Winograd "
+                                      f"level(s)) over {world} GPUs (NCCL p2p), local schedule {lv}",
+                       "makespan_bound": makespan_bound(world, 7 ** levels)},
             "parity": parity, "clocks": clk.summary(),
         }))
 

@@ -1,4 +1,4 @@
-"""Multi-GPU product partition of the top Winograd level.
+"""Multi-GPU product partition of the top one or two Winograd levels.
 
 One process per GPU.  The root rank holds A, B, C.  The top level uses the
 Table-1 (std2) formulas:
@@ -9,7 +9,10 @@ Table-1 (std2) formulas:
     T1 = B12-B11  T2 = B22-T1  T3 = B22-B12  T4 = T2-B21
     C11 = P1+P2   C12 = P1+P6+P5+P3   C21 = P1+P6+P7-P4   C22 = P1+P6+P7+P5
 
-Product i is owned by rank i mod G.  The root forms each remote product's
+With two levels the same formulas are applied again to each S_i / T_i, giving
+49 products P_(i,j) of quarter size; P_(i,j) folds into sub-quadrant q2 of C
+quadrant q1 with coefficient C_COEF[i][q1] * C_COEF[j][q2].  Product t is owned
+by rank t mod G.  The root forms each remote product's
 operands (S_i, T_i) and sends them (point-to-point, NCCL over NVLink on GPUs);
 every rank computes its products with the single-GPU memory-lean plan of the
 local schedule (C-ABI run_variant); the P_i come back to the root, which folds
@@ -119,10 +122,51 @@ class CudaBackend:
                             beta % self.m)
 
 
-def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, root: int = 0):
-    """C <- alpha*A*B + beta*C with the 7 top-level products spread over the
-    ranks of `group`.  A, B, C are only read on the root; other ranks pass
-    None (their shapes are broadcast).  Returns the products computed locally."""
+def product_indices(levels: int) -> List[Tuple[int, ...]]:
+    """The 7^levels products of `levels` Winograd levels, as index tuples
+    (outer level first), in the order they are assigned to ranks."""
+    out: List[Tuple[int, ...]] = [()]
+    for _ in range(levels):
+        out = [t + (i,) for t in out for i in range(7)]
+    return out
+
+
+def _operand(M, idx, coef, backend):
+    """S_idx(A) / T_idx(B) through the levels: quadrant combination of the
+    previous level's operand."""
+    X = M
+    for i in idx:
+        X = backend.lincomb(coef[i], quads(X))
+    return X
+
+
+def _target(acc_quads, idx):
+    """(accumulator block, coefficient) a product P_idx folds into: P_(i1,i2)
+    adds C_COEF[i1][q1] * C_COEF[i2][q2] * P to sub-quadrant q2 of quadrant q1."""
+    out = []
+    for q1 in range(4):
+        c1 = C_COEF[idx[0]][q1]
+        if not c1:
+            continue
+        if len(idx) == 1:
+            out.append((acc_quads[q1], c1))
+            continue
+        for q2 in range(4):
+            c2 = C_COEF[idx[1]][q2]
+            if c2:
+                out.append((quads(acc_quads[q1])[q2], c1 * c2))
+    return out
+
+
+def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, root: int = 0,
+                         levels: int = 1):
+    """C <- alpha*A*B + beta*C with the 7^levels products of the top `levels`
+    Winograd levels (7 or 49) spread over the ranks of `group` (product t on
+    rank t mod G).  A, B, C are only read on the root; other ranks pass None
+    (their shapes are broadcast).  Returns the products computed locally, keyed
+    by their index in product_indices(levels)."""
+    if levels not in (1, 2):
+        raise ValueError("levels must be 1 (7 products) or 2 (49 products)")
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     meta = torch.zeros(4, dtype=torch.int64)
@@ -135,46 +179,44 @@ def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, ro
     m, k, n = (int(x) for x in meta[:3].tolist())
     if rank != root:
         dev = meta.device if meta.is_cuda else torch.device("cpu")
-    h_m, h_k, h_n = m // 2, k // 2, n // 2
-    mine = [i for i in range(7) if owner(i, world) == rank]
+    f = 2 ** levels
+    b_m, b_k, b_n = m // f, k // f, n // f
+    prods = product_indices(levels)
+    mine = [t for t in range(len(prods)) if owner(t, world) == rank]
 
     if rank == root:
-        Aq, Bq = quads(A), quads(B)
-        acc = [torch.zeros((h_m, h_n), dtype=A.dtype, device=dev) for _ in range(4)]
+        acc = [torch.zeros((m // 2, n // 2), dtype=A.dtype, device=dev) for _ in range(4)]
         # operands of remote products go out first so remote ranks start early
         reqs, keep = [], []
-        for i in range(7):
-            o = owner(i, world)
+        for t, idx in enumerate(prods):
+            o = owner(t, world)
             if o == root:
                 continue
-            X = backend.lincomb(S_COEF[i], Aq)
-            Y = backend.lincomb(T_COEF[i], Bq)
+            X = _operand(A, idx, S_COEF, backend)
+            Y = _operand(B, idx, T_COEF, backend)
             keep += [X, Y]
             reqs.append(dist.isend(X, dst=o, group=group))
             reqs.append(dist.isend(Y, dst=o, group=group))
         # post every product receive now: a remote rank may finish its first
         # product before the root has handed out all operands
         pending = []
-        for i in range(7):
-            o = owner(i, world)
+        for t, idx in enumerate(prods):
+            o = owner(t, world)
             if o == root:
                 continue
-            P = torch.empty((h_m, h_n), dtype=A.dtype, device=dev)
-            pending.append((i, P, dist.irecv(P, src=o, group=group)))
+            P = torch.empty((b_m, b_n), dtype=A.dtype, device=dev)
+            pending.append((idx, P, dist.irecv(P, src=o, group=group)))
         local = {}
-        for i in mine:
-            X = backend.lincomb(S_COEF[i], Aq)
-            Y = backend.lincomb(T_COEF[i], Bq)
-            P = backend.product(X, Y)
-            local[i] = P
-            for q in range(4):
-                if C_COEF[i][q]:
-                    backend.fold(acc[q], C_COEF[i][q], P)
-        for i, P, req in pending:
+        for t in mine:
+            idx = prods[t]
+            P = backend.product(_operand(A, idx, S_COEF, backend), _operand(B, idx, T_COEF, backend))
+            local[t] = P
+            for blk, coef in _target(acc, idx):
+                backend.fold(blk, coef, P)
+        for idx, P, req in pending:
             req.wait()
-            for q in range(4):
-                if C_COEF[i][q]:
-                    backend.fold(acc[q], C_COEF[i][q], P)
+            for blk, coef in _target(acc, idx):
+                backend.fold(blk, coef, P)
         for r in reqs:
             r.wait()
         Cq = quads(C)
@@ -182,13 +224,13 @@ def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, ro
             backend.finish(Cq[q], acc[q], alpha, beta)
         return local
     local = {}
-    for i in mine:
-        X = torch.empty((h_m, h_k), dtype=torch.float64, device=dev)
-        Y = torch.empty((h_k, h_n), dtype=torch.float64, device=dev)
+    for t in mine:
+        X = torch.empty((b_m, b_k), dtype=torch.float64, device=dev)
+        Y = torch.empty((b_k, b_n), dtype=torch.float64, device=dev)
         dist.recv(X, src=root, group=group)
         dist.recv(Y, src=root, group=group)
         P = backend.product(X, Y)
-        local[i] = P
+        local[t] = P
         dist.send(P, dst=root, group=group)
     return local
 
@@ -206,3 +248,10 @@ def makespan_bound(world: int, products: int = 7) -> float:
     """Ideal speed-up of the partition in product units."""
     per = -(-products // world)
     return products / per
+
+
+def choose_levels(world: int) -> int:
+    """7 products when they already fill the ranks as well as 49 would (G = 1,
+    7, 8: same makespan, fewer and larger products); 49 otherwise (G = 2: 1.96x
+    instead of 1.75x, G = 4: 3.77x instead of 3.5x)."""
+    return 1 if makespan_bound(world, 7) >= makespan_bound(world, 49) else 2

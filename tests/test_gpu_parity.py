@@ -267,12 +267,12 @@ def test_partition_single_rank_gpu(W, O):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
                             world_size=1, device_id=torch.device("cuda", 0))
     try:
-        for variant, n, cutoff, al, be in [("std2", 512, 64, 1, 0), ("std2", 1024, 128, 3, 7),
-                                           ("ipmm", 512, 64, 1, 0)]:
+        for variant, n, cutoff, al, be, lv in [("std2", 512, 64, 1, 0, 1), ("std2", 1024, 128, 3, 7, 1),
+                                               ("ipmm", 512, 64, 1, 0, 1), ("std2", 1024, 64, 3, 7, 2)]:
             A, B, C = _problem(W, n, n, n, 31 + n, be != 0)
             a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
             be_ = CudaBackend(65521, variant, cutoff, 0)
-            partitioned_multiply(A.t, B.t, C.t, al, be, be_)
+            partitioned_multiply(A.t, B.t, C.t, al, be, be_, levels=lv)
             torch.cuda.synchronize()
             assert (C.to_u32() == O.classical_modp(a0, b0, c0, al, be)).all(), (variant, n)
     finally:
