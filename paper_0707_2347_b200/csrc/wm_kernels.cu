@@ -13,44 +13,12 @@
 #include "wm_launch.h"
 #include "wm_device.h"
 #include "wm_fused.h"
+#include "wm_apply.cuh"
 
 namespace wm {
 
 bool g_pdl = true;
 namespace {
-
-template <bool REAL>
-__device__ __forceinline__ double apply(double a, double b, std::uint32_t mode, double sa,
-                                        double sb, double p, double pinv) {
-    if (REAL) {
-        switch (mode) {
-            case M_ADD: return a + b;
-            case M_SUB: return a - b;
-            case M_RSUB: return b - a;
-            case M_NEGADD: return -(a + b);
-            case M_GEN: return fma(sa, a, sb * b);
-            case M_COPY: return a;
-            case M_NEG: return -a;
-            default: return sa * a;
-        }
-    }
-    double v;
-    switch (mode) {
-        case M_ADD: v = a + b; return v >= p ? v - p : v;
-        case M_SUB: v = a - b; return v < 0.0 ? v + p : v;
-        case M_RSUB: v = b - a; return v < 0.0 ? v + p : v;
-        case M_NEGADD: v = a + b; v = v >= p ? v - p : v; return v != 0.0 ? p - v : 0.0;
-        case M_COPY: return a;
-        case M_NEG: return a != 0.0 ? p - a : 0.0;
-        case M_GEN: v = fma(sa, a, sb * b); break;
-        default: v = sa * a; break;
-    }
-    // v is an exact non-negative integer < 2^53
-    const double q = floor(v * pinv);
-    double r = fma(-q, p, v);
-    r = r < 0.0 ? r + p : r;
-    return r >= p ? r - p : r;
-}
 
 template <bool REAL, int ILP>
 __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
@@ -114,13 +82,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
 
 }  // namespace
 
-namespace fused {
-template <bool REAL>
-__device__ __forceinline__ double gop(std::uint32_t mode, double a, double b, double sa,
-                                      double sb, double p, double pinv) {
-    return apply<REAL>(a, b, mode, sa, sb, p, pinv);
-}
-}  // namespace fused
+
 
 namespace {
 

@@ -211,6 +211,8 @@ struct wm_ctx {
     bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
+    bool post_fold = false;     // fold the parent's next additions into a frame's combine
+                                // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
     const void* traced = nullptr;  // CachedPlan of the last traced run
     bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
@@ -707,6 +709,71 @@ void apply_fold(const Plan& plan, const Fold& fd, double* const base[4], Step& p
     (void)f;
 }
 
+// ---- folding the parent's next additions into a frame's combine --------------
+//
+// When the parent schedule continues with a run of additions over blocks of the
+// frame's output shape (std2 rows 13-18 after P1 = A11 B11 -> X: U2 = P1 + P6,
+// U3 = U2 + P7, ...), the combine thread that writes the frame's four output
+// positions runs that dataflow on the same positions right away: one launch and
+// one round trip of the product through HBM fewer.  Every view of the run must
+// be the frame's output itself or disjoint from it, and disjoint from the
+// product planes other threads of the combine still read.
+void post_fold(const Plan& plan, std::size_t oi, double* const base[4], std::vector<char>& folded,
+               Step& comb) {
+    const Op& F = plan.ops[oi];
+    std::size_t j1 = oi + 1;
+    while (j1 < plan.ops.size() && is_add(plan.ops[j1]) && plan.ops[j1].frame == F.frame &&
+           F.frame >= 0 && !folded[j1])
+        ++j1;
+    const std::size_t r = j1 - (oi + 1);
+    if (r == 0) return;
+    auto ok_view = [&](const View& v) {
+        if (v.rows != F.d.rows || v.cols != F.d.cols) return false;
+        if (!v.same_window(F.d) && v.phys_overlaps(F.d)) return false;
+        for (const View* h : {&F.h0, &F.h1, &F.h2})
+            if (h->rows && v.phys_overlaps(*h)) return false;
+        return v.ld % 2 == 0 && v.cols % 2 == 0;
+    };
+    for (std::size_t j = oi + 1; j < j1; ++j) {
+        const Op& o = plan.ops[j];
+        if (!ok_view(o.d) || !ok_view(o.a) || (o.kind == OP_ADDSUB && !ok_view(o.b))) return;
+    }
+    FramePost& Q = comb.fcomb.post;
+    std::memset(&Q, 0, sizeof(Q));
+    const Field& f = plan.field;
+    if (r == 1) {
+        const Op& o = plan.ops[oi + 1];
+        Q.kind = 2;
+        Q.d = base[o.d.region] + o.d.off;
+        Q.a = base[o.a.region] + o.a.off;
+        Q.b = o.kind == OP_ADDSUB ? base[o.b.region] + o.b.off : Q.a;
+        Q.ldd = o.d.ld;
+        Q.lda = o.a.ld;
+        Q.ldb = o.kind == OP_ADDSUB ? o.b.ld : o.a.ld;
+        Q.mode = o.kind == OP_ADDSUB ? modp_add_mode(f, o.sa, o.sb)
+                                     : (f.is_one(o.sa) ? M_COPY : f.is_minus_one(o.sa) ? M_NEG : M_SCALE);
+        Q.sa = static_cast<double>(o.sa.r);
+        Q.sb = static_cast<double>(o.sb.r);
+        if (!aligned16(Q.d) || !aligned16(Q.a) || !aligned16(Q.b)) {
+            Q.kind = 0;
+            return;
+        }
+    } else {
+        const int g = find_group(plan, oi + 1, folded);
+        Step gs{};
+        if (g < 0 || fused::kGroups[g].nins != static_cast<int>(r) ||
+            !try_group(plan, oi + 1, g, base, gs))
+            return;
+        Q.kind = 1;
+        Q.gid = g;
+        Q.g = gs.grp;
+    }
+    for (std::size_t j = oi + 1; j < j1; ++j) {
+        folded[j] = 1;
+        op_sets(plan.ops[j], comb.rd, comb.wr);
+    }
+}
+
 // Lower an operation list to launches.  Additions are merged into one launch
 // while they are pairwise independent (no write of one touches a read or
 // write of another) and contiguous in program order.
@@ -802,6 +869,8 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 for (std::size_t j = first; j < steps.size(); ++j)
                     if (steps[j].kind == Step::FPREP || steps[j].kind == Step::FCOOP)
                         apply_fold(plan, folds[oi], base, steps[j]);
+            if (ctx.post_fold && !f.real && steps.back().kind == Step::FCOMB)
+                post_fold(plan, oi, base, folded, steps.back());
             continue;
         }
         Step s{};
@@ -1080,6 +1149,12 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
             if (s.kind == Step::FCOMB || s.kind == Step::FCOOP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fcomb.c) * s.fcomb.c;
                 r->frame_comb_bytes += 7 * c2 * 2 + (s.fcomb.beta ? c2 * 8 : 0) + 4 * c2 * sizeof(double);
+                const FramePost& Q = s.fcomb.post;  // folded run: slots over 4 c^2 positions
+                if (Q.kind == 1)
+                    r->frame_comb_bytes += static_cast<std::uint64_t>(fused::kGroups[Q.gid].nload +
+                                                                      fused::kGroups[Q.gid].nstore) *
+                                           4 * c2 * sizeof(double);
+                if (Q.kind == 2) r->frame_comb_bytes += 3 * 4 * c2 * sizeof(double);
             }
             if (s.kind == Step::GROUP) {
                 const fused::GroupDesc& G = fused::kGroups[s.gid];
@@ -1203,7 +1278,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1486,6 +1561,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "fold") ctx->fold = value != 0;
         else if (k == "coop_frames") ctx->coop_frames = value != 0;
         else if (k == "stream_io") ctx->stream_io = value != 0;
+        else if (k == "post_fold") ctx->post_fold = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1510,6 +1586,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "fold") *value = ctx->fold;
         else if (k == "coop_frames") *value = ctx->coop_frames;
         else if (k == "stream_io") *value = ctx->stream_io;
+        else if (k == "post_fold") *value = ctx->post_fold;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
