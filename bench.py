@@ -388,17 +388,20 @@ def main():
         "frame_prep": {"bound": "hbm", "kernel": "k_frame_prep_limbs (S/T + raw limb planes)",
                        "algorithmic_bytes_per_step": rep.frame_prep_bytes,
                        "seconds_per_step": frame_parts.get("prep", 0.0)},
-        "frame_gemm": {"bound": "hbm", "kernel": "k_gemm_direct (7 leaf products per launch)",
+        "frame_gemm": {"bound": "tensor", "kernel": "k_gemm_direct (7 leaf products per launch, "
+                                                    "tcgen05 kind::i8 on 2 x u8 limbs)",
                        "algorithmic_bytes_per_step": rep.frame_gemm_bytes,
                        "seconds_per_step": frame_parts.get("gemm", 0.0),
-                       "int8_ops_per_step": 4 * rep.frame_leaf_flops},
+                       "algorithmic_ops_per_step": 4 * rep.frame_leaf_flops},
         "frame_comb": {"bound": "hbm", "kernel": "k_frame_comb (U-chain, alpha/beta)",
                        "algorithmic_bytes_per_step": rep.frame_comb_bytes,
                        "seconds_per_step": frame_parts.get("comb", 0.0)},
         "leaf_products": {"bound": "tensor",
                           "kernel": ("k_leaf_dmma (float64 DMMA leaves)" if real else
                                      "k_gemm_tma / k_gemm_i8 (unfused int8-limb leaves)"),
-                          "algorithmic_bytes_per_step": None, "seconds_per_step": t_leaf},
+                          "algorithmic_bytes_per_step": None, "seconds_per_step": t_leaf,
+                          "algorithmic_ops_per_step": (rep.leaf_flops - rep.frame_leaf_flops) *
+                                                      (1 if real else 4)},
         "fused_frames": {"bound": "hbm",
                          "kernel": "fused leaf frames (prep + GEMM + comb, three launches)",
                          "algorithmic_bytes_per_step": rep.frame_bytes,
@@ -411,9 +414,10 @@ def main():
         if r_["bound"] == "tensor":
             # float64: 2mnk DMMA flops vs measured cuBLAS DGEMM; mod p: 4 x 2mnk
             # int8 limb ops vs measured cuBLASLt int8
-            ops = (rep.leaf_flops - rep.frame_leaf_flops) * (1 if real else 4)
+            ops = r_["algorithmic_ops_per_step"]
             pk = tpk.get("fp64_tflops" if real else "int8_tops")
-            r_["algorithmic_ops_per_step"] = ops
+            if b and t:  # the operand / product plane stream it also moves
+                r_["achieved_bytes_gbs"] = b / t / 1e9
             r_["achieved"] = ops / t / 1e12 if t and ops else None
             r_["peak"] = pk
             r_["unit"] = "TFLOP/s" if real else "TOP/s"
@@ -424,10 +428,6 @@ def main():
         r_["peak"] = hbm
         r_["unit"] = "GB/s"
         r_["frac"] = r_["achieved"] / hbm if r_["achieved"] else None
-    if rooflines["frame_gemm"]["seconds_per_step"] and tpk.get("int8_tops"):
-        g_ = rooflines["frame_gemm"]
-        g_["tensor_achieved_tops"] = g_["int8_ops_per_step"] / g_["seconds_per_step"] / 1e12
-        g_["tensor_frac"] = g_["tensor_achieved_tops"] / tpk["int8_tops"]
     single = [k_ for k_ in rooflines if k_ != "fused_frames"]
     dominant = max(single, key=lambda k_: rooflines[k_]["seconds_per_step"] or 0.0)
     dom = rooflines[dominant]
@@ -444,6 +444,7 @@ def main():
             "traffic_unit": "dram bytes per step (class total, ncu capture)",
             "peak_source": dom.get("peak_source") or hbm_src, "class": dominant,
             "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
+            "algorithmic_ops_per_step": dom.get("algorithmic_ops_per_step"),
             "kernel_seconds_per_step": dom["seconds_per_step"]}
 
     out = {
