@@ -47,9 +47,100 @@ __global__ void k_chain(const double2* __restrict__ src, double2* __restrict__ d
     for (int i = 0; i < nout; ++i) dst[t + i * stride] = make_double2(acc.x + i, acc.y);
 }
 
+// the same step with a counter handoff instead of griddepcontrol.wait: thread 0
+// spins until the predecessor's CTAs have all signalled, every CTA signals its
+// own completion (release) after its stores
+__global__ void k_chain_flag(const double2* __restrict__ src, double2* __restrict__ dst, int nin,
+                             int nout, std::uint64_t stride, const unsigned* wait_ctr,
+                             unsigned target, unsigned* done_ctr) {
+    if (wait_ctr) {
+        if (threadIdx.x == 0) {
+            unsigned v;
+            unsigned long long t0, t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(wait_ctr) : "memory");
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                if (t - t0 > 2000000000ull) __trap();
+            } while (v < target);
+        }
+        __syncthreads();
+    } else {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    }
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    const std::uint64_t t = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    double2 acc = make_double2(0, 0);
+    for (int i = 0; i < nin; ++i) {
+        const double2 v = src[t + i * stride];
+        acc.x += v.x;
+        acc.y += v.y;
+    }
+    for (int i = 0; i < nout; ++i) dst[t + i * stride] = make_double2(acc.x + i, acc.y);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(done_ctr) : "memory");
+    }
+}
+
 }  // namespace
 
 extern "C" {
+
+// wm_diag_chain with the counter handoff (k_chain_flag)
+int wm_diag_chain_flag(int threads, int block, int nin, int nout, int n, int nbuf, double* us) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 12;
+    const std::uint64_t stride = static_cast<std::uint64_t>(threads);
+    const std::uint64_t words = stride * (nin > nout ? nin : nout);
+    double2* buf = nullptr;
+    unsigned* ctr = nullptr;
+    if (cudaMalloc(&buf, 2 * nbuf * words * sizeof(double2) + 16) != cudaSuccess) return 12;
+    if (cudaMalloc(&ctr, (n + 1) * sizeof(unsigned)) != cudaSuccess) return 12;
+    cudaMemset(buf, 0, 2 * nbuf * words * sizeof(double2));
+    const unsigned nblk = static_cast<unsigned>((threads + block - 1) / block);
+    cudaGraph_t g;
+    cudaGraphExec_t ge;
+    cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    cudaMemsetAsync(ctr, 0, (n + 1) * sizeof(unsigned), s);
+    for (int i = 0; i < n; ++i) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(nblk);
+        cfg.blockDim = dim3(block);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = i > 0 ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const int b = i % nbuf;
+        cudaLaunchKernelEx(&cfg, k_chain_flag, static_cast<const double2*>(buf + 2 * b * words),
+                           buf + (2 * b + 1) * words, nin, nout, stride,
+                           static_cast<const unsigned*>(i > 0 ? ctr + i : nullptr), nblk, ctr + i + 1);
+    }
+    cudaStreamEndCapture(s, &g);
+    if (cudaGraphInstantiate(&ge, g, 0) != cudaSuccess) return 12;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaGraphLaunch(ge, s);
+    cudaStreamSynchronize(s);
+    cudaEventRecord(e0, s);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+    cudaEventRecord(e1, s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *us = 1000.0 * ms / (reps * n);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaFree(buf);
+    cudaFree(ctr);
+    cudaStreamDestroy(s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 12;
+}
 
 // Microseconds per kernel of a PDL chain of `n` k_chain launches (graph replay):
 // `threads` threads each reading nin and writing nout 16-B words, rotating over
