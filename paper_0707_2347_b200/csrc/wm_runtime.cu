@@ -211,6 +211,7 @@ struct wm_ctx {
     bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
+    bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
     bool post_fold = false;     // fold the parent's next additions into a frame's combine
                                 // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
@@ -709,6 +710,88 @@ void apply_fold(const Plan& plan, const Fold& fd, double* const base[4], Step& p
     (void)f;
 }
 
+// ---- product planes in dead blocks -------------------------------------------
+//
+// A fused frame writes its seven product planes into two c x c blocks and its
+// combine reads them back.  By default those are the frame's two temporaries,
+// which every sibling frame of the same parent reuses: the next sibling's GEMM
+// then waits for this frame's combine.  Any other pair of c x c blocks whose
+// content is dead at the frame (the next access in plan order overwrites them
+// whole) serves as well; the latest-overwritten such pair breaks that chain.
+
+// `outer` contains `in` (same region and leading dimension)
+bool view_contains(const View& outer, const View& in) {
+    if (outer.region != in.region || outer.ld != in.ld || in.off < outer.off || outer.empty()) return false;
+    const std::uint64_t d = in.off - outer.off, r0 = d / outer.ld, c0 = d % outer.ld;
+    return r0 + in.rows <= outer.rows && c0 + in.cols <= outer.cols;
+}
+
+// Index of the next plan op after `i` that accesses `w` if that access
+// overwrites all of `w` without reading it; -1 if `w` is live after op i.
+long next_cover(const Plan& plan, std::size_t i, const View& w) {
+    for (std::size_t k = i + 1; k < plan.ops.size(); ++k) {
+        const Op& o = plan.ops[k];
+        const bool acc_like = (o.kind == OP_MUL || o.kind == OP_FRAME) && !plan.field.is_zero(o.sb);
+        if (o.a.phys_overlaps(w)) return -1;
+        if ((o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) && o.b.phys_overlaps(w)) return -1;
+        if (o.kind == OP_FRAME)
+            for (const View* h : {&o.h0, &o.h1, &o.h2})
+                if (h->rows && h->phys_overlaps(w)) return -1;
+        if (o.d.phys_overlaps(w)) return !acc_like && view_contains(o.d, w) ? static_cast<long>(k) : -1;
+    }
+    return -1;  // reaches the end: caller memory stays live, temporaries are not worth it
+}
+
+bool choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
+                          const std::vector<std::size_t>& parent_ops, View* w0, View* w1) {
+    const Op& F = plan.ops[i];
+    const std::uint64_t c = F.a.rows / 2;
+    std::vector<View> excl = {F.a, F.b, F.d, F.h0, F.h1, F.h2};
+    if (fd)
+        for (int w = 0; w < 2; ++w)
+            if (fd->op[w] >= 0) {
+                const Op& o = plan.ops[fd->op[w]];
+                excl.push_back(o.a), excl.push_back(o.b), excl.push_back(o.d);
+            }
+    // the next fused frame must not depend on this combine through the hosts
+    std::size_t next_frame = plan.ops.size();
+    for (std::size_t k = i + 1; k < plan.ops.size(); ++k)
+        if (plan.ops[k].kind == OP_FRAME) {
+            next_frame = k;
+            break;
+        }
+    std::vector<std::pair<long, View>> cand;
+    auto consider = [&](const View& v) {
+        if (v.empty() || v.rows % c || v.cols % c || v.ld % 2) return;
+        for (std::uint64_t r = 0; r < v.rows; r += c)
+            for (std::uint64_t q = 0; q < v.cols; q += c) {
+                const View w = v.window(r, q, c, c);
+                bool clash = false;
+                for (const View& x : excl) clash = clash || (x.rows && x.phys_overlaps(w));
+                for (const auto& e : cand) clash = clash || e.second.phys_overlaps(w);
+                if (clash) continue;
+                const long nc = next_cover(plan, i, w);
+                if (nc > static_cast<long>(next_frame)) cand.push_back({nc, w});
+            }
+    };
+    // blocks of the parent frame's own slots (its quadrants and temporaries)
+    if (F.frame < 0) return false;
+    for (std::size_t k : parent_ops) {
+        const Op& o = plan.ops[k];
+        consider(o.d);
+        consider(o.a);
+        if (o.kind != OP_COPY) consider(o.b);
+    }
+    if (cand.size() < 2) return false;
+    std::stable_sort(cand.begin(), cand.end(),
+                     [](const std::pair<long, View>& x, const std::pair<long, View>& y) {
+                         return x.first > y.first;
+                     });
+    *w0 = cand[0].second;
+    *w1 = cand[1].second;
+    return true;
+}
+
 // ---- folding the parent's next additions into a frame's combine --------------
 //
 // When the parent schedule continues with a run of additions over blocks of the
@@ -829,6 +912,10 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
     for (const Fold& fd : folds)
         for (int w = 0; w < 2; ++w)
             if (fd.op[w] >= 0) folded[fd.op[w]] = 1;
+    std::map<int, std::vector<std::size_t>> by_frame;  // plan ops of each schedule frame
+    if (ctx.dead_hosts)
+        for (std::size_t k = 0; k < plan.ops.size(); ++k)
+            if (plan.ops[k].frame >= 0) by_frame[plan.ops[k].frame].push_back(k);
     for (std::size_t oi = 0; oi < plan.ops.size(); ++oi) {
         const Op& op = plan.ops[oi];
         if (folded[oi]) continue;  // computed by the next frame's prep
@@ -852,7 +939,15 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         flush();
         if (op.kind == OP_FRAME) {
             const std::size_t first = steps.size();
-            lower_frame(op, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
+            Op fop = op;  // product planes in dead blocks when there are some
+            View w0, w1;
+            if (ctx.dead_hosts && !ctx.post_fold && op.frame >= 0 &&
+                choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame], &w0,
+                                     &w1)) {
+                fop.h0 = w0;
+                fop.h1 = w1;
+            }
+            lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
                         ctx.direct_ok && ctx.direct_frames, ctx.multicast);
             if (ctx.coop_frames && steps.size() == first + 3 && steps[first + 1].engine == 2 &&
                 frame_coop_supported(steps[first + 1].fgemm, steps[first + 1].bn)) {
@@ -864,7 +959,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 steps.resize(first);
                 steps.push_back(co);
             }
-            frame_sets(op, f, steps, first);
+            frame_sets(fop, f, steps, first);
             if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
                 for (std::size_t j = first; j < steps.size(); ++j)
                     if (steps[j].kind == Step::FPREP || steps[j].kind == Step::FCOOP)
@@ -1278,7 +1373,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1562,6 +1657,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "coop_frames") ctx->coop_frames = value != 0;
         else if (k == "stream_io") ctx->stream_io = value != 0;
         else if (k == "post_fold") ctx->post_fold = value != 0;
+        else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1587,6 +1683,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "coop_frames") *value = ctx->coop_frames;
         else if (k == "stream_io") *value = ctx->stream_io;
         else if (k == "post_fold") *value = ctx->post_fold;
+        else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
