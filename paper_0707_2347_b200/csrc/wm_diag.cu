@@ -88,6 +88,49 @@ __global__ void k_chain_flag(const double2* __restrict__ src, double2* __restric
 
 extern "C" {
 
+// Host -> device copy rate of a pinned rows x cols u32 matrix: mode 0 one
+// contiguous copy, 1 four quadrant 2-D copies, 2 two contiguous row halves.
+// Returns GB/s.
+int wm_diag_h2d(const void* host, unsigned long long rows, unsigned long long cols, int mode,
+                int reps, double* gbs) {
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return 12;
+    void* dev = nullptr;
+    const std::size_t bytes = rows * cols * 4;
+    if (cudaMalloc(&dev, bytes) != cudaSuccess) return 12;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto once = [&]() {
+        const char* h = static_cast<const char*>(host);
+        char* d = static_cast<char*>(dev);
+        if (mode == 0) {
+            cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
+        } else if (mode == 1) {
+            for (int q = 0; q < 4; ++q) {
+                const std::size_t off = ((q / 2) * (rows / 2) * cols + (q % 2) * (cols / 2)) * 4;
+                cudaMemcpy2DAsync(d + off, cols * 4, h + off, cols * 4, cols / 2 * 4, rows / 2,
+                                  cudaMemcpyHostToDevice, s);
+            }
+        } else {
+            cudaMemcpyAsync(d, h, bytes / 2, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(d + bytes / 2, h + bytes / 2, bytes / 2, cudaMemcpyHostToDevice, s);
+        }
+    };
+    once();
+    cudaStreamSynchronize(s);
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps; ++r) once();
+    cudaEventRecord(e1, s);
+    cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *gbs = static_cast<double>(bytes) * reps / (ms * 1e-3) / 1e9;
+    cudaFree(dev);
+    cudaStreamDestroy(s);
+    return cudaGetLastError() == cudaSuccess ? 0 : 12;
+}
+
 // wm_diag_chain with the counter handoff (k_chain_flag)
 int wm_diag_chain_flag(int threads, int block, int nin, int nout, int n, int nbuf, double* us) {
     cudaStream_t s;

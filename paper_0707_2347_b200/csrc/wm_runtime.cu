@@ -206,8 +206,8 @@ struct wm_ctx {
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
-    int dag = 2;                // concurrent issue over this many streams (0/1: one stream;
-                                // measured: 2 >= 3, 4, 6 > 8 lanes)
+    int dag = 3;                // concurrent issue over this many streams (0/1: one stream;
+                                // measured: 3 >= 2, 4 > 8 lanes)
     bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
@@ -782,6 +782,9 @@ bool choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
         consider(o.a);
         if (o.kind != OP_COPY) consider(o.b);
     }
+    if (std::getenv("WM_HOST_DUMP"))
+        std::fprintf(stderr, "frame %s/%d acc=%d candidates %zu\n", F.sched ? F.sched : "-", F.row,
+                     (int)!plan.field.is_zero(F.sb), cand.size());
     if (cand.size() < 2) return false;
     std::stable_sort(cand.begin(), cand.end(),
                      [](const std::pair<long, View>& x, const std::pair<long, View>& y) {
