@@ -160,6 +160,9 @@ int wm_run_parsed_schedule(wm_ctx* ctx, const char* text, wm_dmat A, wm_dmat B, 
                            uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
 int wm_parse_schedule(const char* text, char* out, int len, int* needed, int* builtin_match);
 int wm_render_schedule(const char* name, char* out, int len, int* needed);
+/* the CostReport run_parsed_schedule would produce (host only, nothing executes) */
+int wm_plan_report_parsed(const char* text, uint32_t p, uint64_t m, uint64_t k, uint64_t n,
+                          uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
 /* Matrix files (ring.hpp:386-449): text "rows cols p" + residues, or binary
  * little-endian u64 (rows, cols, p) + u64 residues.  WM_E_IO on a bad header,
  * a truncated body or a non-canonical entry (read_text / read_binary).

@@ -80,6 +80,8 @@ def ref():
         R.ref_hash.argtypes = [P_u32, u64]
         R.ref_hash.restype = u64
         R.ref_render_builtin.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
+        R.ref_run_parsed.argtypes = [C.c_char_p, u64, u64, u64, u32, P_u32, P_u32, P_u32, u32,
+                                     u32, C.c_int, P_u64, C.c_char_p, C.c_int]
         R.ref_write_matrix.argtypes = [C.c_char_p, C.c_int, u64, u64, u32, C.c_void_p]
         R.ref_read_matrix.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_uint64),
                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint32), C.c_void_p,
@@ -210,3 +212,18 @@ def ref_read_matrix(path, binary=False):
     ref().ref_read_matrix(path.encode(), 1 if binary else 0, C.byref(r), C.byref(c), C.byref(p),
                           out.ctypes.data, out.size)
     return out, p.value
+
+
+def ref_run_parsed(text, A, B, C0, alpha=1, beta=0, cutoff=1, p=DEFAULT_P):
+    """The reference's parse_schedule + run_parsed_schedule -> (C, A, B, report)."""
+    A = np.ascontiguousarray(A, dtype=np.uint32).copy()
+    B = np.ascontiguousarray(B, dtype=np.uint32).copy()
+    Cm = np.ascontiguousarray(C0, dtype=np.uint32).copy()
+    rep = np.zeros(8, dtype=np.uint64)
+    err = C.create_string_buffer(512)
+    rc = ref().ref_run_parsed(text.encode(), A.shape[0], A.shape[1], B.shape[1], p, A.reshape(-1),
+                              B.reshape(-1), Cm.reshape(-1), alpha, beta, cutoff, rep, err, 512)
+    if rc:
+        raise RefError(rc, err.value.decode())
+    return Cm, A, B, dict(zip(["mults", "adds", "peak_extra_words", "total_alloc_words",
+                               "word_moves"], [int(x) for x in rep[:5]]))

@@ -98,6 +98,36 @@ int ref_run_variant(const char* variant, std::uint64_t m, std::uint64_t k,
     }
 }
 
+// run_parsed_schedule (executor.hpp:304-342) of a DSL text with the reference's
+// own parser (schedule.hpp:679-684) on u32 matrices.
+int ref_run_parsed(const char* text, std::uint64_t m, std::uint64_t k, std::uint64_t n,
+                   std::uint32_t p, std::uint32_t* A, std::uint32_t* B, std::uint32_t* C,
+                   std::uint32_t alpha, std::uint32_t beta, int cutoff, std::uint64_t* report_out,
+                   char* err, int errlen) {
+    try {
+        Modulus mod(p);
+        Matrix Am(m, k, mod), Bm(k, n, mod), Cm(m, n, mod);
+        std::memcpy(Am.data(), A, m * k * sizeof(Elem));
+        std::memcpy(Bm.data(), B, k * n * sizeof(Elem));
+        std::memcpy(Cm.data(), C, m * n * sizeof(Elem));
+        CostMeter meter;
+        MultiplyOptions opt;
+        opt.alpha = alpha;
+        opt.beta = beta;
+        opt.cutoff = cutoff;
+        Schedule s = parse_schedule(text);
+        CostReport r = run_parsed_schedule(s, Am, Bm, Cm, opt, &meter);
+        std::memcpy(A, Am.data(), m * k * sizeof(Elem));
+        std::memcpy(B, Bm.data(), k * n * sizeof(Elem));
+        std::memcpy(C, Cm.data(), m * n * sizeof(Elem));
+        fill_report(r, &meter, report_out);
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return code_of(e);
+    }
+}
+
 int ref_expected_costs(const char* variant, std::uint64_t m, std::uint64_t k,
                        std::uint64_t n, int cutoff, std::uint64_t* report_out,
                        char* err, int errlen) {

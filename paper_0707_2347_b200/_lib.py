@@ -26,6 +26,7 @@ EXPORTS = [
     "wm_run_parsed_schedule", "wm_parse_schedule", "wm_render_schedule",
     "wm_run_parsed_schedule_host_u32", "wm_matrix_file_info", "wm_matrix_read_host",
     "wm_matrix_write_host", "wm_matrix_read_device", "wm_matrix_write_device",
+    "wm_plan_report_parsed",
 ]
 
 
@@ -87,6 +88,7 @@ def lib():
                                          i32, P(wm_report)]
     L.wm_parse_schedule.argtypes = [C.c_char_p, C.c_char_p, i32, P(i32), P(i32)]
     L.wm_render_schedule.argtypes = [C.c_char_p, C.c_char_p, i32, P(i32)]
+    L.wm_plan_report_parsed.argtypes = [C.c_char_p, u32, u64, u64, u64, u32, u32, i32, P(wm_report)]
     L.wm_matrix_file_info.argtypes = [C.c_char_p, i32, P(u64), P(u64), P(u32)]
     L.wm_matrix_read_host.argtypes = [C.c_char_p, i32, C.c_void_p, u64]
     L.wm_matrix_write_host.argtypes = [C.c_char_p, i32, u64, u64, u32, C.c_void_p]

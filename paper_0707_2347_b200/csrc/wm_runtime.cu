@@ -1838,6 +1838,21 @@ int wm_plan_report(const char* variant, int field, uint32_t p, uint64_t m, uint6
     });
 }
 
+// The CostReport of run_parsed_schedule for DSL text, without executing.
+int wm_plan_report_parsed(const char* text, uint32_t p, uint64_t m, uint64_t k, uint64_t n,
+                          uint32_t alpha, uint32_t beta, int cutoff, wm_report* report) {
+    return guard([&] {
+        Field f;
+        f.p = p;
+        const Schedule s = parse_schedule(text ? text : "");
+        PlanOptions opt;
+        opt.parsed = &s;
+        Plan plan = plan_variant(s.name, f, m, k, n, k, n, n, modp_scalar(f, alpha),
+                                 modp_scalar(f, beta), cutoff, opt);
+        fill_report(plan, nullptr, report);
+    });
+}
+
 // Diagnostics: dependency DAG of a plan's operations (read / write sets by
 // physical overlap).  out[0] = total cost, out[1] = critical-path cost (cost
 // model: fused frame 9, leaf product 6, block addition 2.5 -- microseconds),

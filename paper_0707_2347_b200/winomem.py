@@ -485,6 +485,15 @@ def parse_schedule(text: str):
     return buf.value.decode(), bool(match.value)
 
 
+def plan_report_parsed(text: str, m, k, n, cutoff=1, alpha=1, beta=0,
+                       p=kDefaultModulus) -> CostReport:
+    """Host-only: the CostReport run_parsed_schedule would produce."""
+    r = wm_report()
+    _check(_lib.lib().wm_plan_report_parsed(text.encode(), p, m, k, n, alpha % p, beta % p,
+                                            cutoff, C.byref(r)))
+    return _report("parsed", m, k, n, cutoff, r)
+
+
 def render_schedule(name: str) -> str:
     """render_schedule (schedule.hpp:617-684) of a builtin schedule."""
     L = _lib.lib()

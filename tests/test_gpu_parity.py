@@ -375,3 +375,22 @@ def test_host_u32_pinned_streamed(W, O, v, n, c, stream_io):
                 assert (A == a0).all() and (B == b0).all()
     finally:
         ctx.set_option("stream_io", saved)
+
+
+def test_run_parsed_hand_written_schedule(W, O):
+    """A non-builtin DSL schedule (tests/test_dsl.py SWAPPED) runs on the device
+    (top frame parsed, children builtin fused frames) bit-exactly, with the
+    reference's run_parsed_schedule meter."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "test_dsl", os.path.join(os.path.dirname(__file__), "test_dsl.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    for (m, k, n, c) in [(1024, 512, 1024, 128), (256, 256, 256, 32)]:
+        A, B, C = _problem(W, m, k, n, 77 + m, False)
+        a0, b0 = A.to_u32(), B.to_u32()
+        rep = W.run_parsed_schedule(mod.SWAPPED, A, B, C, alpha=5, beta=0, cutoff=c)
+        assert (C.to_u32() == O.classical_modp(a0, b0, None, 5, 0)).all(), (m, k, n)
+        plan = W.winomem.plan_report_parsed(mod.SWAPPED, m, k, n, c, 5, 0)
+        assert (rep.mults, rep.adds, rep.peak_extra_words) == (plan.mults, plan.adds,
+                                                              plan.peak_extra_words)
