@@ -56,13 +56,15 @@ def main():
     # last; a launch's time on the path = its end - that predecessor's end, split
     # into the gap before its first CTA started and its own span
     j = int(np.argmax(end))
-    crit, gaps = {}, {}
+    crit, gaps, edges = {}, {}, {}
     path = 0
     while j >= 0:
         preds = [p for p in [prev_on_lane[j]] + [w for w in waits[j] if w >= 0] if p >= 0]
         p = max(preds, key=lambda q: end[q]) if preds else -1
         pe = end[p] if p >= 0 else 0.0
         k_ = KINDS[kind[j]]
+        e_ = (KINDS[kind[p]] if p >= 0 else "-") + ">" + k_
+        edges[e_] = edges.get(e_, 0) + 1
         crit[k_] = crit.get(k_, 0.0) + end[j] - max(start[j], pe)
         gaps[k_] = gaps.get(k_, 0.0) + max(0.0, start[j] - pe)
         path += 1
@@ -79,6 +81,7 @@ def main():
                       "critical_span_us_by_kind": {k_: round(v, 1) for k_, v in crit.items()},
                       "critical_gap_us_by_kind": {k_: round(v, 1) for k_, v in gaps.items()},
                       "span_stats": stats,
+                      "critical_edges": dict(sorted(edges.items(), key=lambda kv: -kv[1])[:12]),
                       "lanes": {int(l): int((lane == l).sum()) for l in np.unique(lane)}}))
 
 
