@@ -123,7 +123,8 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
                 break;
             case Step::FGEMM:
                 add(s.rd, o.d), add(s.wr, o.h0), add(s.wr, o.h1);
-                if (acc) add(s.rd, o.a), add(s.rd, o.b), add(s.rd, o.h2);
+                if (acc) add(s.rd, o.h2);
+                if (acc && !o.h2.rows) add(s.rd, o.b);  // float64 B22 (no plane slot left)
                 break;
             case Step::FCOMB:
                 add(s.rd, o.h0), add(s.rd, o.h1), add(s.rd, o.d), add(s.wr, o.d);
@@ -742,11 +743,15 @@ long next_cover(const Plan& plan, std::size_t i, const View& w) {
     return -1;  // reaches the end: caller memory stays live, temporaries are not worth it
 }
 
-bool choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
-                          const std::vector<std::size_t>& parent_ops, View* w0, View* w1) {
+// Up to `want` windows, best first; `recent` are blocks the previous frames'
+// launches may still be reading (their product / raw plane hosts).
+std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
+                                       const std::vector<std::size_t>& parent_ops,
+                                       const std::vector<View>& recent, std::size_t want) {
     const Op& F = plan.ops[i];
     const std::uint64_t c = F.a.rows / 2;
     std::vector<View> excl = {F.a, F.b, F.d, F.h0, F.h1, F.h2};
+    excl.insert(excl.end(), recent.begin(), recent.end());
     if (fd)
         for (int w = 0; w < 2; ++w)
             if (fd->op[w] >= 0) {
@@ -775,7 +780,7 @@ bool choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
             }
     };
     // blocks of the parent frame's own slots (its quadrants and temporaries)
-    if (F.frame < 0) return false;
+    if (F.frame < 0) return {};
     for (std::size_t k : parent_ops) {
         const Op& o = plan.ops[k];
         consider(o.d);
@@ -785,14 +790,13 @@ bool choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
     if (std::getenv("WM_HOST_DUMP"))
         std::fprintf(stderr, "frame %s/%d acc=%d candidates %zu\n", F.sched ? F.sched : "-", F.row,
                      (int)!plan.field.is_zero(F.sb), cand.size());
-    if (cand.size() < 2) return false;
     std::stable_sort(cand.begin(), cand.end(),
                      [](const std::pair<long, View>& x, const std::pair<long, View>& y) {
                          return x.first > y.first;
                      });
-    *w0 = cand[0].second;
-    *w1 = cand[1].second;
-    return true;
+    std::vector<View> out;
+    for (std::size_t t = 0; t < cand.size() && t < want; ++t) out.push_back(cand[t].second);
+    return out;
 }
 
 // ---- folding the parent's next additions into a frame's combine --------------
@@ -916,6 +920,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         for (int w = 0; w < 2; ++w)
             if (fd.op[w] >= 0) folded[fd.op[w]] = 1;
     std::map<int, std::vector<std::size_t>> by_frame;  // plan ops of each schedule frame
+    std::vector<View> recent_hosts;                    // plane hosts of the previous frame
     if (ctx.dead_hosts)
         for (std::size_t k = 0; k < plan.ops.size(); ++k)
             if (plan.ops[k].frame >= 0) by_frame[plan.ops[k].frame].push_back(k);
@@ -942,13 +947,23 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         flush();
         if (op.kind == OP_FRAME) {
             const std::size_t first = steps.size();
-            Op fop = op;  // product planes in dead blocks when there are some
-            View w0, w1;
-            if (ctx.dead_hosts && !ctx.post_fold && op.frame >= 0 &&
-                choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame], &w0,
-                                     &w1)) {
-                fop.h0 = w0;
-                fop.h1 = w1;
+            Op fop = op;  // product (and raw) planes in dead blocks when there are some
+            if (ctx.dead_hosts && !ctx.post_fold && op.frame >= 0) {
+                // accumulating frames: a third block takes the raw planes, so that
+                // with two temporaries B22 is materialised too and the GEMM no
+                // longer reads the frame's B (the parent's next prep rewrites it)
+                const bool acc = !f.is_zero(op.sb);
+                const std::vector<View> w =
+                    choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame],
+                                         recent_hosts, acc ? 3 : 2);
+                if (w.size() >= 2) {
+                    fop.h0 = w[0];
+                    fop.h1 = w[1];
+                    if (acc && w.size() >= 3) fop.h2 = w[2];
+                }
+                // the next frames keep off this frame's plane hosts
+                recent_hosts.assign({fop.h0, fop.h1});
+                if (fop.h2.rows) recent_hosts.push_back(fop.h2);
             }
             lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
                         ctx.direct_ok && ctx.direct_frames, ctx.multicast);
