@@ -21,7 +21,7 @@ KINDS = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "COOP"]
 
 def main():
     import torch
-    name = sys.argv[1] if len(sys.argv) > 1 else "C2"
+    name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "C2"
     cfg = bench.CONFIGS[name]
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
     A, B, Cm = W.Matrix(m, k), W.Matrix(k, n), W.Matrix(m, n)
@@ -33,6 +33,17 @@ def main():
     ctx.set_option("trace", 1)
     run = lambda: W.run_variant(cfg["variant"], A, B, Cm, alpha=cfg["alpha"], beta=cfg["beta"],
                                 cutoff=cfg["cutoff"])
+    if "--e2e" in sys.argv:  # the host boundary streamed through the graph (pinned u32)
+        from oracle import oracle as O
+        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+        hA, hB = pin(O.fill_random(m, k, cfg["seed"])), pin(O.fill_random(k, n, cfg["seed"] + 1))
+        hC = pin(O.fill_random(m, n, cfg["seed"] + 2))
+        import time
+
+        def run():
+            t0 = time.perf_counter()
+            W.run_variant_host(cfg["variant"], hA, hB, hC, cfg["alpha"], cfg["beta"], cfg["cutoff"])
+            print("e2e wall ms", round((time.perf_counter() - t0) * 1e3, 3), file=sys.stderr)
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -76,7 +87,11 @@ def main():
     stats = {k_: {"n": len(v), "mean_us": round(float(np.mean(v)), 2),
                   "p50_us": round(float(np.median(v)), 2)} for k_, v in span.items()}
     busy = crit
+    timed = start >= 0
+    first_compute = float(start[timed].min()) if timed.any() else -1.0
     print(json.dumps({"config": name, "launches": int(n_), "step_us": float(end.max()),
+                      "first_kernel_start_us": first_compute,
+                      "untimed_launches": int((~timed).sum()),
                       "critical_launches": path,
                       "critical_span_us_by_kind": {k_: round(v, 1) for k_, v in crit.items()},
                       "critical_gap_us_by_kind": {k_: round(v, 1) for k_, v in gaps.items()},
