@@ -16,7 +16,7 @@ import bench  # noqa: E402
 import paper_0707_2347_b200 as W  # noqa: E402
 from paper_0707_2347_b200._lib import lib  # noqa: E402
 
-KINDS = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "COOP"]
+KINDS = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "COOP", "UPLOAD", "DOWNLOAD"]
 
 
 def main():
