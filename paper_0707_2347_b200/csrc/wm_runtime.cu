@@ -115,7 +115,6 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
     };
     for (std::size_t j = first; j < steps.size(); ++j) {
         Step& s = steps[j];
-        if (std::getenv("WM_OLD_SETS")) { op_sets(o, s.rd, s.wr); continue; }
         switch (s.kind) {
             case Step::FPREP:
                 add(s.rd, o.a), add(s.rd, o.b), add(s.rd, o.d), add(s.wr, o.d);
@@ -608,13 +607,6 @@ std::vector<Fold> plan_folds(const Plan& plan) {
         // the complete run of the parent's additions just before the frame
         std::size_t j0 = i;
         while (j0 > 0 && is_add(plan.ops[j0 - 1]) && plan.ops[j0 - 1].frame == F.frame) --j0;
-        if (std::getenv("WM_FOLD_DUMP")) {
-            std::fprintf(stderr, "frame %s/%d run %zu:", F.sched ? F.sched : "-", F.row, i - j0);
-            for (std::size_t j = j0; j < i; ++j)
-                std::fprintf(stderr, " %d%s", plan.ops[j].row,
-                             plan.ops[j].d.same_window(F.a) ? "a" : plan.ops[j].d.same_window(F.b) ? "b" : "-");
-            std::fprintf(stderr, "\n");
-        }
         if (j0 == i) continue;
         const bool acc = F.sb.r != 0;
         // what the prep itself writes (the GEMM's product planes in h0 / h1 come later)
@@ -674,11 +666,6 @@ std::vector<Fold> plan_folds(const Plan& plan) {
         // an accumulating frame with two temporaries has no plane slot left for
         // B22: its GEMM reads that block of B as float64 (lower_frame)
         if (acc && !F.h2.rows) fd.writeback[1] = true;
-        if (std::getenv("WM_FOLD_DUMP"))
-            std::fprintf(stderr, "  -> fold a=%d(wb %d) b=%d(wb %d) acc=%d h2=%d\n",
-                         fd.op[0] >= 0 ? plan.ops[fd.op[0]].row : 0, (int)fd.writeback[0],
-                         fd.op[1] >= 0 ? plan.ops[fd.op[1]].row : 0, (int)fd.writeback[1], (int)acc,
-                         (int)(F.h2.rows != 0));
         folds[i] = fd;
     }
     return folds;
@@ -787,9 +774,6 @@ std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fo
         consider(o.a);
         if (o.kind != OP_COPY) consider(o.b);
     }
-    if (std::getenv("WM_HOST_DUMP"))
-        std::fprintf(stderr, "frame %s/%d acc=%d candidates %zu\n", F.sched ? F.sched : "-", F.row,
-                     (int)!plan.field.is_zero(F.sb), cand.size());
     std::stable_sort(cand.begin(), cand.end(),
                      [](const std::pair<long, View>& x, const std::pair<long, View>& y) {
                          return x.first > y.first;
