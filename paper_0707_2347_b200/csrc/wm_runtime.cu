@@ -212,6 +212,7 @@ struct wm_ctx {
     bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
     bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
+    int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool post_fold = false;     // fold the parent's next additions into a frame's combine
                                 // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
@@ -1375,7 +1376,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1424,7 +1425,8 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     if (dag && !cp->dag)
         cp->dag = std::make_shared<DagPlan>(plan_dag(
             cp->steps, std::max(1, ctx->dag),
-            io ? std::max(kEpoch, std::min<int>(4096, static_cast<int>(cp->steps.size()))) : kEpoch));
+            io ? std::max(ctx->epoch, std::min<int>(4096, static_cast<int>(cp->steps.size())))
+               : ctx->epoch));
     if (ctx->trace) {
         // [start, end] globaltimer slots per launch, patched into the launch
         // parameters of this (trace-keyed) plan before its graph is captured
@@ -1660,6 +1662,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "stream_io") ctx->stream_io = value != 0;
         else if (k == "post_fold") ctx->post_fold = value != 0;
         else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
+        else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1686,6 +1689,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "stream_io") *value = ctx->stream_io;
         else if (k == "post_fold") *value = ctx->post_fold;
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
+        else if (k == "epoch") *value = ctx->epoch;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
