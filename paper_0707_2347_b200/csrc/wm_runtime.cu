@@ -691,10 +691,14 @@ void apply_fold(const Plan& plan, const Fold& fd, double* const base[4], Step& p
         ff.sa = static_cast<double>(o.sa.r);
         ff.on = 1;
         ff.writeback = fd.writeback[w] ? 1 : 0;
-        // dependency sets: the sources are read, the operand view is (re)written
+        // dependency sets: the prep reads the sources instead of the operand view,
+        // and writes the operand view only when it stores it back
+        const View& X = o.d;
+        for (auto it = prep.rd.begin(); it != prep.rd.end();)
+            it = it->same_window(X) ? prep.rd.erase(it) : it + 1;
         prep.rd.push_back(o.a);
         if (o.kind == OP_ADDSUB) prep.rd.push_back(o.b);
-        prep.wr.push_back(o.d);
+        if (ff.writeback) prep.wr.push_back(X);
     }
     (void)f;
 }
