@@ -213,6 +213,7 @@ struct wm_ctx {
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
     bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
+    bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
     bool post_fold = false;     // fold the parent's next additions into a frame's combine
                                 // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
@@ -408,7 +409,7 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, int force, bool direct, bool multicast) {
+                 int engine, int force, bool direct, bool multicast, bool wide_plain) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
@@ -521,6 +522,11 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     if (direct) {
         g.bn = (force >= 1000 && force < 3000) ? force % 1000 + 1000 * (force / 1000 - 1)
                                                 : gemm_direct_choose(G);
+        // plain frames overlap their siblings (product planes in dead blocks):
+        // half the CTAs at twice the width leave SMs to the sibling launches
+        // (measured: config 2 4.35 -> 4.23 ms, config 3 15.24 -> 14.35 ms; at
+        // c = 128 the grid is already small and it loses)
+        if (force == 0 && wide_plain && !acc && g.bn == 32 && G.n % 64 == 0 && G.m >= 256) g.bn = 64;
         auto maps = std::make_shared<TmaMaps>();
         gemm_direct_cluster(G, g.bn, multicast);
         if (!gemm_direct_supported(G, g.bn) || !gemm_direct_encode(G, g.bn, *maps))
@@ -955,7 +961,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 if (fop.h2.rows) recent_hosts.push_back(fop.h2);
             }
             lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
-                        ctx.direct_ok && ctx.direct_frames, ctx.multicast);
+                        ctx.direct_ok && ctx.direct_frames, ctx.multicast, ctx.wide_plain);
             if (ctx.coop_frames && steps.size() == first + 3 && steps[first + 1].engine == 2 &&
                 frame_coop_supported(steps[first + 1].fgemm, steps[first + 1].bn)) {
                 // the three launches as phases of one cooperative launch
@@ -1380,7 +1386,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1667,6 +1673,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "post_fold") ctx->post_fold = value != 0;
         else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
+        else if (k == "wide_plain") ctx->wide_plain = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1694,6 +1701,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "post_fold") *value = ctx->post_fold;
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "epoch") *value = ctx->epoch;
+        else if (k == "wide_plain") *value = ctx->wide_plain;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
