@@ -27,6 +27,10 @@
 #include "wm_frame_dev.cuh"
 
 namespace wm {
+
+int g_prep_rows = 1;     // rows per prep CTA ("prep_rows" option)
+unsigned g_comb_block = 128;  // combine CTA size ("comb_block" option)
+
 namespace {
 
 using fdev::rmod;
@@ -122,7 +126,10 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
     WM_TL_BEGIN(P.tl);
-    const std::uint64_t r = blockIdx.x, j = 2 * threadIdx.x;
+    // blockDim = rows * c/2: each CTA owns whole rows (reads precede writes per row)
+    const std::uint32_t half = P.c / 2;
+    const std::uint64_t r = blockIdx.x * (blockDim.x / half) + threadIdx.x / half;
+    const std::uint64_t j = 2 * (threadIdx.x % half);
     fdev::PrepRegs R;
     fdev::prep_limbs_load(P, r, j, R);
     __syncthreads();  // row r of every host has been read before any of it is overwritten
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
 // run of the parent's additions (a separate instantiation keeps the plain
 // combine's registers and code small)
 template <bool POST>
-__global__ void __launch_bounds__(128) k_frame_comb(const FrameCombParams P) {
+__global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
     WM_TL_BEGIN(P.tl);
@@ -169,8 +176,10 @@ cudaError_t launch_pdl(K kern, const Prm& P, std::uint64_t threads, cudaStream_t
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
     if (P.limbs) {
         if (P.c > 2048) return cudaErrorInvalidValue;
+        const unsigned rows = static_cast<unsigned>(g_prep_rows > 0 && P.c / 2 * g_prep_rows <= 1024
+                                                         ? g_prep_rows : 1);
         return launch_pdl(k_frame_prep_limbs, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
-                          P.c / 2);
+                          rows * (P.c / 2));
     }
     return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
 }
@@ -178,7 +187,8 @@ cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s) {
     if (P.post.kind)
         return launch_pdl(k_frame_comb<true>, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
-    return launch_pdl(k_frame_comb<false>, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
+    return launch_pdl(k_frame_comb<false>, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
+                      g_comb_block);
 }
 
 bool frame_kernel_available() { return true; }

@@ -5,6 +5,10 @@ namespace wm {
 // Programmatic dependent launch on every kernel (default on; the "pdl" context
 // option turns it off for measurements).
 extern bool g_pdl;
+// launch shapes of the frame prep / combine (wm_frame.cu; context options
+// "prep_rows", "comb_block")
+extern int g_prep_rows;
+extern unsigned g_comb_block;
 }  // namespace wm
 
 // Where a kernel lets its programmatic dependents launch.  A dependent launched

@@ -1666,6 +1666,8 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "direct_frames") ctx->direct_frames = value != 0;
         else if (k == "dag") ctx->dag = static_cast<int>(value);
         else if (k == "pdl") g_pdl_user = value != 0;
+        else if (k == "prep_rows") g_prep_rows = static_cast<int>(value);
+        else if (k == "comb_block") g_comb_block = static_cast<unsigned>(value);
         else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
         else if (k == "coop_frames") ctx->coop_frames = value != 0;
@@ -1694,6 +1696,8 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "direct_frames") *value = ctx->direct_frames;
         else if (k == "dag") *value = ctx->dag;
         else if (k == "pdl") *value = g_pdl_user;
+        else if (k == "prep_rows") *value = g_prep_rows;
+        else if (k == "comb_block") *value = g_comb_block;
         else if (k == "multicast") *value = ctx->multicast;
         else if (k == "fold") *value = ctx->fold;
         else if (k == "coop_frames") *value = ctx->coop_frames;
