@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cstring>
 #include <list>
@@ -18,6 +19,7 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/winomem_b200.h"
@@ -727,25 +729,51 @@ bool view_contains(const View& outer, const View& in) {
 
 // Index of the next plan op after `i` that accesses `w` if that access
 // overwrites all of `w` without reading it; -1 if `w` is live after op i.
-long next_cover(const Plan& plan, std::size_t i, const View& w) {
-    for (std::size_t k = i + 1; k < plan.ops.size(); ++k) {
-        const Op& o = plan.ops[k];
-        const bool acc_like = (o.kind == OP_MUL || o.kind == OP_FRAME) && !plan.field.is_zero(o.sb);
-        if (o.a.phys_overlaps(w)) return -1;
-        if ((o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) && o.b.phys_overlaps(w)) return -1;
-        if (o.kind == OP_FRAME)
-            for (const View* h : {&o.h0, &o.h1, &o.h2})
-                if (h->rows && h->phys_overlaps(w)) return -1;
-        if (o.d.phys_overlaps(w)) return !acc_like && view_contains(o.d, w) ? static_cast<long>(k) : -1;
+// How plan op `o` accesses `w`: 0 not at all, 1 reads it (or writes part of
+// it), 2 overwrites all of it without reading it.
+int access_kind(const Plan& plan, const Op& o, const View& w) {
+    const bool acc_like = (o.kind == OP_MUL || o.kind == OP_FRAME) && !plan.field.is_zero(o.sb);
+    if (o.a.phys_overlaps(w)) return 1;
+    if ((o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) && o.b.phys_overlaps(w)) return 1;
+    if (o.kind == OP_FRAME)
+        for (const View* h : {&o.h0, &o.h1, &o.h2})
+            if (h->rows && h->phys_overlaps(w)) return 1;
+    if (o.d.phys_overlaps(w)) return !acc_like && view_contains(o.d, w) ? 2 : 1;
+    return 0;
+}
+
+// Every access to each candidate block, computed once per block (physical
+// identity) and shared by all frames of a plan.
+struct AccessIndex {
+    std::map<std::tuple<int, std::uint64_t, std::uint64_t, std::uint64_t, std::uint64_t>,
+             std::vector<std::pair<std::size_t, int>>>
+        acc;
+    const std::vector<std::pair<std::size_t, int>>& of(const Plan& plan, const View& w) {
+        const auto key = std::make_tuple(static_cast<int>(w.region), w.off, w.ld, w.rows, w.cols);
+        auto it = acc.find(key);
+        if (it != acc.end()) return it->second;
+        std::vector<std::pair<std::size_t, int>> v;
+        for (std::size_t k = 0; k < plan.ops.size(); ++k) {
+            const int a = access_kind(plan, plan.ops[k], w);
+            if (a) v.push_back({k, a});
+        }
+        return acc.emplace(key, std::move(v)).first->second;
     }
-    return -1;  // reaches the end: caller memory stays live, temporaries are not worth it
+};
+
+long next_cover(const Plan& plan, std::size_t i, const View& w, AccessIndex& ix) {
+    const auto& v = ix.of(plan, w);
+    auto it = std::upper_bound(v.begin(), v.end(), std::make_pair(i, 3));
+    if (it == v.end()) return -1;  // reaches the end: caller memory stays live
+    return it->second == 2 ? static_cast<long>(it->first) : -1;
 }
 
 // Up to `want` windows, best first; `recent` are blocks the previous frames'
 // launches may still be reading (their product / raw plane hosts).
 std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fold* fd,
                                        const std::vector<std::size_t>& parent_ops,
-                                       const std::vector<View>& recent, std::size_t want) {
+                                       const std::vector<View>& recent, std::size_t want,
+                                       AccessIndex& ix) {
     const Op& F = plan.ops[i];
     const std::uint64_t c = F.a.rows / 2;
     std::vector<View> excl = {F.a, F.b, F.d, F.h0, F.h1, F.h2};
@@ -773,7 +801,7 @@ std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fo
                 for (const View& x : excl) clash = clash || (x.rows && x.phys_overlaps(w));
                 for (const auto& e : cand) clash = clash || e.second.phys_overlaps(w);
                 if (clash) continue;
-                const long nc = next_cover(plan, i, w);
+                const long nc = next_cover(plan, i, w, ix);
                 if (nc > static_cast<long>(next_frame)) cand.push_back({nc, w});
             }
     };
@@ -784,6 +812,19 @@ std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fo
         consider(o.d);
         consider(o.a);
         if (o.kind != OP_COPY) consider(o.b);
+    }
+    // and the blocks of the operations around it (the grandparent's slots):
+    // measured on the launch DAG, a window of 96 operations finds as much as 256
+    {
+        const std::size_t win = 96;
+        const std::size_t lo = i > win ? i - win : 0, hi = std::min(plan.ops.size(), i + win);
+        for (std::size_t k = lo; k < hi; ++k) {
+            const Op& o = plan.ops[k];
+            if (o.frame == F.frame) continue;
+            consider(o.d);
+            consider(o.a);
+            if (o.kind != OP_COPY) consider(o.b);
+        }
     }
     std::stable_sort(cand.begin(), cand.end(),
                      [](const std::pair<long, View>& x, const std::pair<long, View>& y) {
@@ -916,6 +957,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             if (fd.op[w] >= 0) folded[fd.op[w]] = 1;
     std::map<int, std::vector<std::size_t>> by_frame;  // plan ops of each schedule frame
     std::vector<View> recent_hosts;                    // plane hosts of the previous frame
+    AccessIndex access_ix;                             // accesses per candidate block
     if (ctx.dead_hosts)
         for (std::size_t k = 0; k < plan.ops.size(); ++k)
             if (plan.ops[k].frame >= 0) by_frame[plan.ops[k].frame].push_back(k);
@@ -950,7 +992,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 const bool acc = !f.is_zero(op.sb);
                 const std::vector<View> w =
                     choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame],
-                                         recent_hosts, acc ? 3 : 2);
+                                         recent_hosts, acc ? 3 : 2, access_ix);
                 if (w.size() >= 2) {
                     fop.h0 = w[0];
                     fop.h1 = w[1];
