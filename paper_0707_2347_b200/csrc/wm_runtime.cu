@@ -958,6 +958,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
     std::map<int, std::vector<std::size_t>> by_frame;  // plan ops of each schedule frame
     std::vector<View> recent_hosts;                    // plane hosts of the previous frame
     AccessIndex access_ix;                             // accesses per candidate block
+    std::vector<std::vector<View>> host_hist;          // plane hosts of the last frames
     if (ctx.dead_hosts)
         for (std::size_t k = 0; k < plan.ops.size(); ++k)
             if (plan.ops[k].frame >= 0) by_frame[plan.ops[k].frame].push_back(k);
@@ -998,9 +999,13 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                     fop.h1 = w[1];
                     if (acc && w.size() >= 3) fop.h2 = w[2];
                 }
-                // the next frames keep off this frame's plane hosts
-                recent_hosts.assign({fop.h0, fop.h1});
-                if (fop.h2.rows) recent_hosts.push_back(fop.h2);
+                // the next frames keep off the plane hosts of the last `keep` frames
+                const std::size_t keep = 2;  // launch-DAG model: 2 beats 1, 3, 4
+                host_hist.push_back({fop.h0, fop.h1});
+                if (fop.h2.rows) host_hist.back().push_back(fop.h2);
+                while (host_hist.size() > keep) host_hist.erase(host_hist.begin());
+                recent_hosts.clear();
+                for (const auto& hv : host_hist) recent_hosts.insert(recent_hosts.end(), hv.begin(), hv.end());
             }
             lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
                         ctx.direct_ok && ctx.direct_frames, ctx.multicast, ctx.wide_plain);
