@@ -68,6 +68,7 @@ struct FrameCombParams {
     double pd, pinv;
     unsigned long long* tl;     // measurement timeline slot (nullptr: off)
     FramePost post;
+    std::uint32_t cin_f64;      // beta != 0: C_in read as float64 from C (no packing)
 };
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s);

@@ -166,7 +166,17 @@ __device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_
         pv[k][1] = static_cast<double>(w >> 16);
     }
     double cin[2][4];  // [col e][quadrant]
-    if (P.beta != 0) {
+    if (P.beta != 0 && P.cin_f64) {
+        // C kept its float64 C_in (the planes live in dead blocks): this thread
+        // reads exactly the positions it writes
+        const double be = static_cast<double>(P.beta);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+            const double2 x = *reinterpret_cast<const double2*>(P.C.q[qd] + r * P.C.ld + j);
+            cin[0][qd] = rmod(be * x.x, p, pinv);
+            cin[1][qd] = rmod(be * x.y, p, pinv);
+        }
+    } else if (P.beta != 0) {
         const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {

@@ -110,13 +110,26 @@ void op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) {
 //   combine: reads h0, h1 and the packed beta*C_in in C;  writes C
 constexpr std::uint8_t kGridRegion = 200;  // pseudo region: "all SMs" (cooperative frames)
 
-void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size_t first) {
+void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size_t first,
+                const View* ext = nullptr) {
     const bool acc = !f.is_zero(o.sb);
     auto add = [](std::vector<View>& s, const View& v) {
         if (v.rows) s.push_back(v);
     };
     for (std::size_t j = first; j < steps.size(); ++j) {
         Step& s = steps[j];
+        if (ext && s.kind != Step::FCOOP) {  // planes outside C: the prep never touches C
+            if (s.kind == Step::FPREP) {
+                add(s.rd, o.a), add(s.rd, o.b);
+                for (int e = 0; e < 4; ++e) add(s.wr, ext[e]);
+            } else if (s.kind == Step::FGEMM) {
+                for (int e = 0; e < 4; ++e) add(s.rd, ext[e]);
+                add(s.wr, o.h0), add(s.wr, o.h1);
+            } else if (s.kind == Step::FCOMB) {
+                add(s.rd, o.h0), add(s.rd, o.h1), add(s.rd, o.d), add(s.wr, o.d);
+            }
+            continue;
+        }
         switch (s.kind) {
             case Step::FPREP:
                 add(s.rd, o.a), add(s.rd, o.b), add(s.rd, o.d), add(s.wr, o.d);
@@ -132,6 +145,8 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
                 break;
             case Step::FCOOP: {
                 op_sets(o, s.rd, s.wr);
+                if (ext)
+                    for (int e = 0; e < 4; ++e) add(s.wr, ext[e]);
                 // one cooperative frame at a time: its grid needs every SM
                 View grid;
                 grid.region = kGridRegion;
@@ -216,6 +231,7 @@ struct wm_ctx {
     bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
+    bool cin_direct = true;     // accumulating frames: all planes in dead blocks, C_in read by the combine
     bool post_fold = false;     // fold the parent's next additions into a frame's combine
                                 // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
@@ -411,13 +427,16 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, int force, bool direct, bool multicast, bool wide_plain) {
+                 int engine, int force, bool direct, bool multicast, bool wide_plain,
+                 const View* ext = nullptr) {
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
     const bool acc = !f.is_zero(op.sb);
-    const View& sh = acc ? cq[1] : cq[0];  // S planes host
-    const View& th = acc ? cq[2] : cq[1];  // T planes host
+    // ext (accumulating frames with dead blocks to spare): S / T planes in ext[0]
+    // / ext[1], raw planes in ext[2], ext[3]; C keeps C_in untouched for the combine
+    const View& sh = ext ? ext[0] : acc ? cq[1] : cq[0];  // S planes host
+    const View& th = ext ? ext[1] : acc ? cq[2] : cq[1];  // T planes host
     // direct-limb engine: operand planes are limb pairs (hi / lo byte rows) that
     // the GEMM loads straight into tensor-core layout; prep CTAs own whole rows
     direct = direct && c <= 2048;
@@ -466,7 +485,10 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     // accumulating frame is left in float64 (a B operand: the direct engine
     // splits it in the GEMM).
     std::vector<std::pair<View, int>> raw_slots;
-    if (!acc) {
+    if (ext) {
+        for (int q = 0; q < 4; ++q) raw_slots.push_back({ext[2], q});
+        for (int q = 0; q < 2; ++q) raw_slots.push_back({ext[3], q});
+    } else if (!acc) {
         for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[2], q});
         for (int q = 0; q < 4; ++q) raw_slots.push_back({cq[3], q});
     } else {
@@ -496,7 +518,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
         p.fprep.pld[PL_S1 + i] = st[i].ld;
     }
     p.fprep.c = static_cast<std::uint32_t>(c);
-    p.fprep.beta = op.sb.r;
+    p.fprep.beta = ext ? 0 : op.sb.r;  // ext: nothing to pack, C is not touched
     p.fprep.pd = pd;
     p.fprep.pinv = pinv;
     steps.push_back(p);
@@ -552,6 +574,7 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     cb.fcomb.c = static_cast<std::uint32_t>(c);
     cb.fcomb.alpha = op.sa.r;
     cb.fcomb.beta = op.sb.r;
+    cb.fcomb.cin_f64 = ext ? 1 : 0;
     cb.fcomb.pd = pd;
     cb.fcomb.pinv = pinv;
     steps.push_back(cb);
@@ -986,6 +1009,8 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
         if (op.kind == OP_FRAME) {
             const std::size_t first = steps.size();
             Op fop = op;  // product (and raw) planes in dead blocks when there are some
+            View ext[4];
+            bool use_ext = false;
             if (ctx.dead_hosts && !ctx.post_fold && op.frame >= 0) {
                 // accumulating frames: a third block takes the raw planes, so that
                 // with two temporaries B22 is materialised too and the GEMM no
@@ -993,22 +1018,30 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 const bool acc = !f.is_zero(op.sb);
                 const std::vector<View> w =
                     choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame],
-                                         recent_hosts, acc ? 3 : 2, access_ix);
+                                         recent_hosts, acc ? 6 : 2, access_ix);
                 if (w.size() >= 2) {
                     fop.h0 = w[0];
                     fop.h1 = w[1];
-                    if (acc && w.size() >= 3) fop.h2 = w[2];
+                    if (acc && w.size() >= 6 && ctx.cin_direct) {
+                        // every plane outside C: the prep neither reads nor packs C_in
+                        for (int e = 0; e < 4; ++e) ext[e] = w[2 + e];
+                        use_ext = true;
+                    } else if (acc && w.size() >= 3) {
+                        fop.h2 = w[2];
+                    }
                 }
                 // the next frames keep off the plane hosts of the last `keep` frames
                 const std::size_t keep = 2;  // launch-DAG model: 2 beats 1, 3, 4
                 host_hist.push_back({fop.h0, fop.h1});
                 if (fop.h2.rows) host_hist.back().push_back(fop.h2);
+                if (use_ext) host_hist.back().insert(host_hist.back().end(), ext, ext + 4);
                 while (host_hist.size() > keep) host_hist.erase(host_hist.begin());
                 recent_hosts.clear();
                 for (const auto& hv : host_hist) recent_hosts.insert(recent_hosts.end(), hv.begin(), hv.end());
             }
             lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
-                        ctx.direct_ok && ctx.direct_frames, ctx.multicast, ctx.wide_plain);
+                        ctx.direct_ok && ctx.direct_frames, ctx.multicast, ctx.wide_plain,
+                        use_ext ? ext : nullptr);
             if (ctx.coop_frames && steps.size() == first + 3 && steps[first + 1].engine == 2 &&
                 frame_coop_supported(steps[first + 1].fgemm, steps[first + 1].bn)) {
                 // the three launches as phases of one cooperative launch
@@ -1019,7 +1052,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 steps.resize(first);
                 steps.push_back(co);
             }
-            frame_sets(fop, f, steps, first);
+            frame_sets(fop, f, steps, first, use_ext ? ext : nullptr);
             if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
                 for (std::size_t j = first; j < steps.size(); ++j)
                     if (steps[j].kind == Step::FPREP || steps[j].kind == Step::FCOOP)
@@ -1433,7 +1466,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1723,6 +1756,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "wide_plain") ctx->wide_plain = value != 0;
+        else if (k == "cin_direct") ctx->cin_direct = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
@@ -1753,6 +1787,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;
+        else if (k == "cin_direct") *value = ctx->cin_direct;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else if (k == "frame_cfg") *value = ctx->frame_cfg;
