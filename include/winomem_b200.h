@@ -102,10 +102,23 @@ const char* wm_last_error(void);
 int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out);
 int wm_ctx_destroy(wm_ctx* ctx);
 int wm_ctx_sync(wm_ctx* ctx);
-/* options: "fuse_frames" (0/1), "graphs" (0/1), "batch_adds" (0/1),
- *          "leaf_kernel" (0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto),
- *          "subset" (measurement only: 0 all launches, 1 additions only,
- *                    2 leaf products only, 3 fused frames only) */
+/* options (defaults in brackets; every change drops the cached plans):
+ *   "fuse_frames" [1]   fused leaf frames (prep / seven-product GEMM / combine)
+ *   "graphs" [1]        capture each plan once into a CUDA graph
+ *   "batch_adds" [1], "fuse_adds" [1]   batched / generated fused addition runs
+ *   "fold" [1]          operand-producing additions folded into the frame prep
+ *   "dead_hosts" [1]    frame planes in dead blocks (plan liveness)
+ *   "cin_direct" [1]    accumulating frames: all planes outside C, C_in read by the combine
+ *   "wide_plain" [1]    plain frames' GEMM at BN = 64 (c >= 256)
+ *   "dag" [3]           issue lanes (concurrent streams); "epoch" [512] launches per join
+ *   "stream_io" [1]     host u32 boundary streamed through the graph (pinned buffers)
+ *   "leaf_kernel" [2]   0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto
+ *   "direct_frames" [1], "gemm_engine" [0], "multicast" [0], "frame_cfg" [0]   GEMM engines
+ *   "coop_frames" [0], "post_fold" [0]   measured-slower alternatives
+ *   "pdl" [1], "prep_rows" [1], "comb_block" [128]   launch attributes / shapes
+ *   "trace" [0]         per-launch timeline (wm_diag_trace)
+ *   "subset" [0]        measurement only: 0 all launches, 1 additions only,
+ *                       2 leaf products only, 3 fused frames, 4/5/6 frame prep/GEMM/combine */
 int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value);
 int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value);
 
