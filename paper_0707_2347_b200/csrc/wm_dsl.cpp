@@ -16,6 +16,7 @@
 // Untagged products recurse into std2 (no accumulator term) or acc3.  The
 // device executes scalars +-1, alpha and beta; an integer literal other than 1
 // is rejected at parse time.
+#include <algorithm>
 #include <cctype>
 #include <map>
 #include <sstream>
@@ -25,71 +26,27 @@
 namespace wm {
 namespace {
 
-struct Tok {
-    enum Kind { Ident, Int, Sym, End } kind = End;
-    std::string text;
-    long long value = 0;
+// ------------------------------------------------------------------ tables
+
+// recursion tags (schedule.hpp:109-121) <-> this build's schedule names
+struct TagName {
+    const char* text;
+    const char* target;
 };
-
-class Lexer {
-  public:
-    Lexer(const std::string& s, int line) : s_(s), line_(line) {}
-    Tok peek() {
-        if (!has_) cur_ = lex(), has_ = true;
-        return cur_;
-    }
-    Tok next() {
-        Tok t = peek();
-        has_ = false;
-        return t;
-    }
-    [[noreturn]] void error(const std::string& m) const {
-        fail(E_PARSE, "line " + std::to_string(line_) + ": " + m);
-    }
-    int line() const { return line_; }
-
-  private:
-    Tok lex() {
-        while (pos_ < s_.size() && std::isspace(static_cast<unsigned char>(s_[pos_]))) ++pos_;
-        if (pos_ >= s_.size() || s_[pos_] == '#') return {};
-        const char c = s_[pos_];
-        const std::size_t b = pos_;
-        if (std::isdigit(static_cast<unsigned char>(c))) {
-            while (pos_ < s_.size() && std::isdigit(static_cast<unsigned char>(s_[pos_]))) ++pos_;
-            const std::string t = s_.substr(b, pos_ - b);
-            return {Tok::Int, t, std::stoll(t)};
-        }
-        if (std::isalpha(static_cast<unsigned char>(c))) {
-            while (pos_ < s_.size() && (std::isalnum(static_cast<unsigned char>(s_[pos_])) ||
-                                        s_[pos_] == '_' || s_[pos_] == '\''))
-                ++pos_;
-            return {Tok::Ident, s_.substr(b, pos_ - b), 0};
-        }
-        ++pos_;
-        return {Tok::Sym, std::string(1, c), 0};
-    }
-    std::string s_;
-    int line_;
-    std::size_t pos_ = 0;
-    Tok cur_;
-    bool has_ = false;
-};
-
-// recursion tags (schedule.hpp:109-121) -> this build's schedule names
-const char* const kTagNames[] = {"Classic", "Std2", "Acc3", "IP",   "OvL", "OvR",
-                                 "AcLR",    "AccR", "Acc2", "AcR", "Self"};
-const char* const kTagTargets[] = {"classic", "std2", "acc3", "ip",  "ovl", "ovr",
-                                   "aclr",    "accr", "acc2", "acr", "self"};
+constexpr TagName kTags[] = {{"Classic", "classic"}, {"Std2", "std2"}, {"Acc3", "acc3"},
+                             {"IP", "ip"},           {"OvL", "ovl"},   {"OvR", "ovr"},
+                             {"AcLR", "aclr"},       {"AccR", "accr"}, {"Acc2", "acc2"},
+                             {"AcR", "acr"},         {"Self", "self"}};
 
 const char* tag_target(const std::string& t) {
-    for (int i = 0; i < 11; ++i)
-        if (t == kTagNames[i]) return kTagTargets[i];
+    for (const TagName& e : kTags)
+        if (t == e.text) return e.target;
     return nullptr;
 }
 
 const char* tag_display(const std::string& target) {
-    for (int i = 0; i < 11; ++i)
-        if (target == kTagTargets[i]) return kTagNames[i];
+    for (const TagName& e : kTags)
+        if (target == e.target) return e.text;
     return nullptr;
 }
 
@@ -102,238 +59,300 @@ bool slot_by_name(const std::string& t, Slot* out) {
     return false;
 }
 
+struct DimName {
+    Dim d;
+    const char* text;
+};
+constexpr DimName kDims[] = {{Dim::M2, "m/2"},
+                             {Dim::K2, "k/2"},
+                             {Dim::N2, "n/2"},
+                             {Dim::MaxK2N2, "max(k/2,n/2)"},
+                             {Dim::MaxM2K2, "max(m/2,k/2)"}};
+
 bool dim_by_name(const std::string& t, Dim* d) {
-    if (t == "m/2") *d = Dim::M2;
-    else if (t == "k/2") *d = Dim::K2;
-    else if (t == "n/2") *d = Dim::N2;
-    else if (t == "max(k/2,n/2)") *d = Dim::MaxK2N2;
-    else if (t == "max(m/2,k/2)") *d = Dim::MaxM2K2;
-    else return false;
-    return true;
+    for (const DimName& e : kDims)
+        if (t == e.text) {
+            *d = e.d;
+            return true;
+        }
+    return false;
 }
 
 const char* dim_text(Dim d) {
-    switch (d) {
-        case Dim::M2: return "m/2";
-        case Dim::K2: return "k/2";
-        case Dim::N2: return "n/2";
-        case Dim::MaxK2N2: return "max(k/2,n/2)";
-        case Dim::MaxM2K2: return "max(m/2,k/2)";
-    }
+    for (const DimName& e : kDims)
+        if (e.d == d) return e.text;
     return "?";
 }
 
-struct Term {
-    Sym sym;
-    bool is_prod = false;
-    Slot a = SX, b = SX;
-    std::string tag;            // recursion call (empty: none)
-    std::vector<Term> inner;    // its terms
-    bool scalar_outside = false;
+// ------------------------------------------------------------------ tokens
+
+// One source line cut into words (identifiers, integers) and single-character
+// punctuation; everything after '#' is a comment.
+struct Piece {
+    enum Kind : std::uint8_t { Word, Number, Punct } kind;
+    std::string text;
 };
 
-using Labels = std::map<std::string, Slot>;
-
-Slot resolve(const Labels& L, const std::string& t, const Lexer& lx) {
-    auto it = L.find(t);
-    if (it == L.end())
-        fail(E_UNKNOWN_SLOT, "line " + std::to_string(lx.line()) + ": unknown operand '" + t + "'");
-    return it->second;
-}
-
-std::vector<Term> parse_terms(const Labels& L, Lexer& lx) {
-    std::vector<Term> out;
-    bool first = true;
-    for (;;) {
-        Tok t = lx.peek();
-        if (t.kind == Tok::End || (t.kind == Tok::Sym && (t.text == "@" || t.text == ")"))) break;
-        Term term;
-        if (t.kind == Tok::Sym && (t.text == "+" || t.text == "-")) {
-            term.sym.neg = t.text == "-";
-            lx.next();
-        } else if (!first) {
-            lx.error("expected '+' or '-' between terms");
+std::vector<Piece> cut_line(const std::string& line) {
+    std::vector<Piece> out;
+    std::size_t i = 0;
+    auto is_word = [](char ch) {
+        return std::isalnum(static_cast<unsigned char>(ch)) || ch == '_' || ch == '\'';
+    };
+    while (i < line.size()) {
+        const char ch = line[i];
+        if (ch == '#') break;
+        if (std::isspace(static_cast<unsigned char>(ch))) {
+            ++i;
+            continue;
         }
-        first = false;
-        Tok u = lx.peek();
-        bool scaled = false;
-        if (u.kind == Tok::Int) {
-            if (u.value != 1) lx.error("integer scalars other than 1 are not supported on the device path");
-            lx.next();
-            scaled = true;
-        } else if (u.kind == Tok::Ident && (u.text == "alpha" || u.text == "beta")) {
-            term.sym.sym = u.text == "alpha" ? 1 : 2;
-            lx.next();
-            scaled = true;
-        }
-        if (scaled) {
-            Tok star = lx.next();
-            if (star.kind != Tok::Sym || star.text != "*") lx.error("expected '*' after scalar");
-        }
-        Tok id = lx.next();
-        if (id.kind != Tok::Ident) lx.error("expected operand");
-        const char* target = tag_target(id.text);
-        Tok paren = lx.peek();
-        if (target && paren.kind == Tok::Sym && paren.text == "(") {
-            lx.next();
-            term.tag = target;
-            term.scalar_outside = scaled;
-            term.inner = parse_terms(L, lx);
-            Tok close = lx.next();
-            if (close.kind != Tok::Sym || close.text != ")") lx.error("expected ')'");
+        std::size_t j = i + 1;
+        if (std::isdigit(static_cast<unsigned char>(ch))) {
+            while (j < line.size() && std::isdigit(static_cast<unsigned char>(line[j]))) ++j;
+            out.push_back({Piece::Number, line.substr(i, j - i)});
+        } else if (std::isalpha(static_cast<unsigned char>(ch))) {
+            while (j < line.size() && is_word(line[j])) ++j;
+            out.push_back({Piece::Word, line.substr(i, j - i)});
         } else {
-            term.a = resolve(L, id.text, lx);
-            Tok star = lx.peek();
-            if (star.kind == Tok::Sym && star.text == "*") {
-                lx.next();
-                Tok id2 = lx.next();
-                if (id2.kind != Tok::Ident) lx.error("expected operand after '*'");
-                term.b = resolve(L, id2.text, lx);
-                term.is_prod = true;
-            }
+            out.push_back({Piece::Punct, std::string(1, ch)});
         }
-        out.push_back(term);
+        i = j;
     }
     return out;
 }
 
-bool parse_directive(Schedule& s, Lexer& lx, const std::string& raw) {
-    const std::string kw = lx.peek().text;
-    if (kw != "schedule" && kw != "contract" && kw != "accumulating" && kw != "shape" && kw != "temp")
-        return false;
-    lx.next();
-    if (kw == "schedule") {
-        s.name = lx.next().text;
-    } else if (kw == "contract") {
+// ------------------------------------------------------------------ header
+
+// Header lines precede the first instruction; the dimension expressions of a
+// `temp` line are whitespace-separated words of the raw line.
+bool read_header_line(Schedule& s, const std::string& raw, int line) {
+    std::istringstream words(raw);
+    std::string key;
+    words >> key;
+    auto bad = [&](const std::string& m) { fail(E_PARSE, "line " + std::to_string(line) + ": " + m); };
+    if (key == "schedule") {
+        words >> s.name;
+    } else if (key == "contract") {
         std::string v;
-        for (Tok t = lx.next(); t.kind != Tok::End; t = lx.next()) v += t.text;
-        if (v == "read-only") s.contract = Contract::ReadOnly;
-        else if (v == "overwrite-A") s.contract = Contract::OverwriteA;
-        else if (v == "overwrite-B") s.contract = Contract::OverwriteB;
-        else if (v == "overwrite-both") s.contract = Contract::OverwriteBoth;
-        else lx.error("unknown contract: " + v);
-    } else if (kw == "accumulating") {
-        const std::string v = lx.next().text;
-        if (v != "true" && v != "false") lx.error("accumulating expects true|false");
+        words >> v;
+        const Contract all[] = {Contract::ReadOnly, Contract::OverwriteA, Contract::OverwriteB,
+                                Contract::OverwriteBoth};
+        bool known = false;
+        for (Contract c : all)
+            if (v == contract_name(c)) s.contract = c, known = true;
+        if (!known) bad("unknown contract: " + v);
+    } else if (key == "accumulating") {
+        std::string v;
+        words >> v;
+        if (v != "true" && v != "false") bad("accumulating expects true|false");
         s.accumulating = v == "true";
-    } else if (kw == "shape") {
-        const std::string v = lx.next().text;
-        if (v == "square") s.square_only = true;
-        else if (v == "rectangular") s.square_only = false;
-        else lx.error("shape expects square|rectangular");
+    } else if (key == "shape") {
+        std::string v;
+        words >> v;
+        if (v != "square" && v != "rectangular") bad("shape expects square|rectangular");
+        s.square_only = v == "square";
+    } else if (key == "temp") {
+        std::string slot, rows, cols;
+        words >> slot >> rows >> cols;
+        TempDecl t{};
+        if (!slot_by_name(slot, &t.slot) || slot_role(t.slot) != Role::Temporary)
+            bad("temp expects a temporary slot name");
+        if (!dim_by_name(rows, &t.rows) || !dim_by_name(cols, &t.cols)) bad("bad temp dimension");
+        s.temps.push_back(t);
     } else {
-        std::istringstream ts(raw);
-        std::string w, slot, rd, cd;
-        ts >> w >> slot >> rd >> cd;
-        Slot sl;
-        Dim r, c;
-        if (!slot_by_name(slot, &sl) || slot_role(sl) != Role::Temporary)
-            lx.error("temp expects a temporary slot name");
-        if (!dim_by_name(rd, &r) || !dim_by_name(cd, &c)) lx.error("bad temp dimension");
-        s.temps.push_back({sl, r, c});
+        return false;
     }
     return true;
 }
 
-void parse_instruction(Schedule& s, Labels& L, Lexer& lx) {
-    Tok idx = lx.next();
-    if (idx.kind != Tok::Int) lx.error("expected instruction index");
-    if (idx.value != static_cast<long long>(s.ins.size()) + 1)
-        lx.error("instruction indices must be sequential from 1");
-    Tok colon = lx.next();
-    if (colon.kind != Tok::Sym || colon.text != ":") lx.error("expected ':'");
-    Tok lbl = lx.next();
-    if (lbl.kind != Tok::Ident) lx.error("expected result label");
-    Tok eq = lx.next();
-    if (eq.kind != Tok::Sym || eq.text != "=") lx.error("expected '='");
-    std::vector<Term> terms = parse_terms(L, lx);
-    Tok at = lx.next();
-    if (at.kind != Tok::Sym || at.text != "@") lx.error("expected '@ SLOT'");
-    Tok dt = lx.next();
-    Slot dst;
-    if (dt.kind != Tok::Ident || !slot_by_name(dt.text, &dst))
-        fail(E_UNKNOWN_SLOT, "line " + std::to_string(lx.line()) + ": unknown destination slot");
-    if (lx.peek().kind != Tok::End) lx.error("trailing tokens");
+// ------------------------------------------------------------------ body
 
-    Instr in;
-    in.dst = dst;
-    bool have_prod = false;
-    std::vector<Term> adds;
-    for (const Term& t : terms) {
-        if (!t.tag.empty()) {
-            if (have_prod) lx.error("more than one product term");
-            bool found = false;
-            for (const Term& u : t.inner) {
-                if (!u.tag.empty()) lx.error("nested recursion tags");
-                if (u.is_prod) {
-                    if (found) lx.error("two products in one call");
-                    found = true;
-                    Sym ps = u.sym;
-                    if (t.scalar_outside) {
-                        if (t.inner.size() != 1)
-                            lx.error("a scalar before a tagged call needs a pure product inside");
-                        if (t.sym.neg) ps.neg = !ps.neg;
-                        if (t.sym.sym) {
-                            if (ps.sym) lx.error("conflicting scalars");
-                            ps.sym = t.sym.sym;
-                        }
-                    } else if (t.sym.neg) {
-                        ps.neg = !ps.neg;
-                    }
-                    in.s0 = ps;
-                    in.o0 = u.a;
-                    in.o1 = u.b;
-                } else {
-                    adds.push_back(u);
+// A right-hand side is a signed sum of terms; a term is an operand, a product
+// of two operands, or a recursion call Tag(...) around such a sum.
+struct Term {
+    Sym sym;
+    enum Form : std::uint8_t { Operand, Product, Call } form = Operand;
+    Slot lhs = SX, rhs = SX;
+    std::string target;        // Call: recursion target
+    std::vector<Term> inside;  // Call: its terms
+    bool prefixed = false;     // Call: scalar written before the tag
+};
+
+class InstructionReader {
+  public:
+    InstructionReader(std::vector<Piece> pieces, int line, std::map<std::string, Slot>& names)
+        : p_(std::move(pieces)), line_(line), names_(names) {}
+
+    void read_into(Schedule& s) {
+        const long long index = number("expected instruction index");
+        if (index != static_cast<long long>(s.ins.size()) + 1)
+            error("instruction indices must be sequential from 1");
+        punct(':', "expected ':'");
+        const std::string label = word("expected result label");
+        punct('=', "expected '='");
+        const std::vector<Term> sum = terms();
+        punct('@', "expected '@ SLOT'");
+        Slot dst;
+        if (!looking_at(Piece::Word) || !slot_by_name(p_[i_].text, &dst))
+            fail(E_UNKNOWN_SLOT, "line " + std::to_string(line_) + ": unknown destination slot");
+        ++i_;
+        if (i_ != p_.size()) error("trailing tokens");
+
+        Instr in = lower(sum);
+        in.dst = dst;
+        if (!slot_writable(dst, s.contract))
+            fail(E_CONTRACT_VIOLATION, "line " + std::to_string(line_) + ": writing " +
+                                           slot_name(dst) + " violates contract " +
+                                           contract_name(s.contract));
+        if (slot_role(dst) == Role::Temporary &&
+            std::none_of(s.temps.begin(), s.temps.end(), [&](const TempDecl& t) { return t.slot == dst; }))
+            s.temps.push_back({dst, Dim::N2, Dim::N2});
+        names_[label] = dst;
+        s.ins.push_back(in);
+    }
+
+  private:
+    [[noreturn]] void error(const std::string& m) const {
+        fail(E_PARSE, "line " + std::to_string(line_) + ": " + m);
+    }
+    bool looking_at(Piece::Kind k, char ch = 0) const {
+        return i_ < p_.size() && p_[i_].kind == k && (!ch || p_[i_].text[0] == ch);
+    }
+    void punct(char ch, const char* m) {
+        if (!looking_at(Piece::Punct, ch)) error(m);
+        ++i_;
+    }
+    std::string word(const char* m) {
+        if (!looking_at(Piece::Word)) error(m);
+        return p_[i_++].text;
+    }
+    long long number(const char* m) {
+        if (!looking_at(Piece::Number)) error(m);
+        return std::stoll(p_[i_++].text);
+    }
+    Slot operand(const std::string& name) const {
+        const auto it = names_.find(name);
+        if (it == names_.end())
+            fail(E_UNKNOWN_SLOT, "line " + std::to_string(line_) + ": unknown operand '" + name + "'");
+        return it->second;
+    }
+
+    std::vector<Term> terms() {
+        std::vector<Term> out;
+        while (i_ < p_.size() && !looking_at(Piece::Punct, '@') && !looking_at(Piece::Punct, ')')) {
+            Term t;
+            if (looking_at(Piece::Punct, '+') || looking_at(Piece::Punct, '-'))
+                t.sym.neg = p_[i_++].text[0] == '-';
+            else if (!out.empty())
+                error("expected '+' or '-' between terms");
+            bool scaled = false;
+            if (looking_at(Piece::Number)) {
+                if (p_[i_].text != "1") error("integer scalars other than 1 are not supported on the device path");
+                ++i_;
+                scaled = true;
+            } else if (looking_at(Piece::Word) && (p_[i_].text == "alpha" || p_[i_].text == "beta")) {
+                t.sym.sym = p_[i_++].text == "alpha" ? 1 : 2;
+                scaled = true;
+            }
+            if (scaled) punct('*', "expected '*' after scalar");
+            const std::string head = word("expected operand");
+            const char* target = tag_target(head);
+            if (target && looking_at(Piece::Punct, '(')) {
+                ++i_;
+                t.form = Term::Call;
+                t.target = target;
+                t.prefixed = scaled;
+                t.inside = terms();
+                punct(')', "expected ')'");
+            } else {
+                t.lhs = operand(head);
+                if (looking_at(Piece::Punct, '*')) {
+                    ++i_;
+                    t.rhs = operand(word("expected operand after '*'"));
+                    t.form = Term::Product;
                 }
             }
-            if (!found) lx.error("tagged call without a product");
-            in.tag = t.tag;
-            have_prod = true;
-        } else if (t.is_prod) {
-            if (have_prod) lx.error("more than one product term");
-            in.s0 = t.sym;
-            in.o0 = t.a;
-            in.o1 = t.b;
-            have_prod = true;
-        } else {
-            adds.push_back(t);
+            out.push_back(std::move(t));
         }
+        return out;
     }
-    if (!have_prod && adds.empty()) lx.error("empty right-hand side");
-    if (adds.size() > 2) lx.error("more than two slot terms");
-    if (have_prod && adds.size() > 1) lx.error("a product allows at most one accumulator term");
-    if (have_prod) {
-        in.kind = Instr::Product;
-        if (!adds.empty()) {
-            in.has_acc = true;
-            in.sacc = adds[0].sym;
-            in.oacc = adds[0].a;
+
+    // Terms -> one instruction: at most one product (tagged or not) with at most
+    // one accumulator term, or one / two slot terms.
+    Instr lower(const std::vector<Term>& sum) const {
+        Instr in;
+        const Term* product = nullptr;
+        std::string target;
+        Sym product_sym;
+        std::vector<const Term*> slots;
+        auto take_product = [&](const Term& t, Sym sym, const std::string& tag) {
+            if (product) error("more than one product term");
+            product = &t;
+            product_sym = sym;
+            target = tag;
+        };
+        for (const Term& t : sum) {
+            if (t.form == Term::Operand) {
+                slots.push_back(&t);
+            } else if (t.form == Term::Product) {
+                take_product(t, t.sym, "");
+            } else {
+                if (product) error("more than one product term");
+                const Term* inner_product = nullptr;
+                for (const Term& u : t.inside) {
+                    if (u.form == Term::Call) error("nested recursion tags");
+                    if (u.form == Term::Operand) {
+                        slots.push_back(&u);
+                        continue;
+                    }
+                    if (inner_product) error("two products in one call");
+                    inner_product = &u;
+                }
+                if (!inner_product) error("tagged call without a product");
+                // the call's own sign / scalar distributes onto its product
+                Sym sym = inner_product->sym;
+                if (t.prefixed && t.inside.size() != 1)
+                    error("a scalar before a tagged call needs a pure product inside");
+                sym.neg = sym.neg != t.sym.neg;
+                if (t.prefixed && t.sym.sym) {
+                    if (sym.sym) error("conflicting scalars");
+                    sym.sym = t.sym.sym;
+                }
+                take_product(*inner_product, sym, t.target);
+            }
         }
-        if (in.tag.empty()) in.tag = in.has_acc ? "acc3" : "std2";  // schedule.hpp:583-585
-    } else if (adds.size() == 2) {
-        in.kind = Instr::Add2;
-        in.s0 = adds[0].sym;
-        in.o0 = adds[0].a;
-        in.s1 = adds[1].sym;
-        in.o1 = adds[1].a;
-    } else {
-        in.kind = Instr::Copy1;
-        in.s0 = adds[0].sym;
-        in.o0 = adds[0].a;
+        if (!product && slots.empty()) error("empty right-hand side");
+        if (slots.size() > 2) error("more than two slot terms");
+        if (product) {
+            if (slots.size() > 1) error("a product allows at most one accumulator term");
+            in.kind = Instr::Product;
+            in.s0 = product_sym;
+            in.o0 = product->lhs;
+            in.o1 = product->rhs;
+            in.has_acc = !slots.empty();
+            if (in.has_acc) {
+                in.sacc = slots[0]->sym;
+                in.oacc = slots[0]->lhs;
+            }
+            // untagged products: std2, or acc3 with an accumulator (schedule.hpp:583-585)
+            in.tag = !target.empty() ? target : in.has_acc ? "acc3" : "std2";
+            return in;
+        }
+        in.kind = slots.size() == 2 ? Instr::Add2 : Instr::Copy1;
+        in.s0 = slots[0]->sym;
+        in.o0 = slots[0]->lhs;
+        if (slots.size() == 2) {
+            in.s1 = slots[1]->sym;
+            in.o1 = slots[1]->lhs;
+        }
+        return in;
     }
-    if (!slot_writable(in.dst, s.contract))
-        fail(E_CONTRACT_VIOLATION, "line " + std::to_string(lx.line()) + ": writing " +
-                                       slot_name(in.dst) + " violates contract " +
-                                       contract_name(s.contract));
-    if (slot_role(in.dst) == Role::Temporary) {
-        bool declared = false;
-        for (const auto& t : s.temps) declared |= t.slot == in.dst;
-        if (!declared) s.temps.push_back({in.dst, Dim::N2, Dim::N2});
-    }
-    L[lbl.text] = in.dst;
-    s.ins.push_back(in);
-}
+
+    std::vector<Piece> p_;
+    std::size_t i_ = 0;
+    int line_;
+    std::map<std::string, Slot>& names_;
+};
 
 std::string sym_text(const Sym& s) {
     std::string t = s.neg ? "-" : "";
@@ -348,19 +367,19 @@ Schedule parse_schedule(const std::string& text) {
     Schedule s;  // defaults of schedule.hpp:219-224
     s.name = "anonymous";
     s.square_only = true;
-    Labels L;
-    for (int i = 0; i < NSLOT; ++i) L[slot_name(static_cast<Slot>(i))] = static_cast<Slot>(i);
-    std::istringstream is(text);
+    std::map<std::string, Slot> names;  // slot names, then result labels
+    for (int i = 0; i < NSLOT; ++i) names[slot_name(static_cast<Slot>(i))] = static_cast<Slot>(i);
+    std::istringstream lines(text);
     std::string raw;
     int line = 0;
-    bool saw_ins = false;
-    while (std::getline(is, raw)) {
-        Lexer lx(raw, ++line);
-        const Tok first = lx.peek();
-        if (first.kind == Tok::End) continue;
-        if (first.kind == Tok::Ident && !saw_ins && parse_directive(s, lx, raw)) continue;
-        saw_ins = true;
-        parse_instruction(s, L, lx);
+    bool in_body = false;
+    while (std::getline(lines, raw)) {
+        ++line;
+        std::vector<Piece> pieces = cut_line(raw);
+        if (pieces.empty()) continue;
+        if (!in_body && pieces[0].kind == Piece::Word && read_header_line(s, raw, line)) continue;
+        in_body = true;
+        InstructionReader(std::move(pieces), line, names).read_into(s);
     }
     return s;
 }

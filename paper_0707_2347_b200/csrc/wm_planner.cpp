@@ -133,122 +133,7 @@ void QuadrantWorkspace::pop_frame() {
     frames_.pop_back();
 }
 
-// ------------------------------------------------------------ cost model
-
-namespace {
-
-Costs classical_costs(std::uint64_t m, std::uint64_t k, std::uint64_t n, bool acc) {
-    Costs c;
-    c.mults = m * k * n;
-    c.adds = m * n * (k - 1) + (acc ? m * n : 0);
-    return c;
-}
-
-bool name_accumulates(const std::string& name) {
-    return name == "acc3" || name == "aclr" || name == "accr" || name == "acc2" || name == "acr";
-}
-
-// Evaluator (models.hpp:33-179)
-class Evaluator {
-  public:
-    explicit Evaluator(int cutoff) : cutoff_(cutoff) {}
-
-    Costs schedule(const std::string& name, std::uint64_t m, std::uint64_t k, std::uint64_t n) {
-        auto key = std::make_tuple(name, m, k, n);
-        auto it = memo_.find(key);
-        if (it != memo_.end()) return it->second;
-        Costs c = eval(name, m, k, n);
-        memo_.emplace(key, c);
-        return c;
-    }
-
-    Costs ipmm(std::uint64_t n, std::uint64_t k) {
-        if (n <= static_cast<std::uint64_t>(cutoff_)) return classical_costs(n, k, n, false);
-        const std::uint64_t s = n / 2, q = 2 * k / n;
-        Costs w = schedule("std2", s, s, s), wa = schedule("acc3", s, s, s), rec = ipmm(s, k);
-        Costs r;
-        r.mults = 3 * w.mults + 3 * (q - 1) * wa.mults + rec.mults;
-        r.adds = 3 * w.adds + 3 * (q - 1) * wa.adds + rec.adds;
-        return r;
-    }
-
-  private:
-    Costs eval(const std::string& name, std::uint64_t m, std::uint64_t k, std::uint64_t n) {
-        const bool acc = name_accumulates(name);
-        if (std::min({m, k, n}) <= static_cast<std::uint64_t>(cutoff_))
-            return classical_costs(m, k, n, acc);
-        const std::uint64_t m2 = m / 2, k2 = k / 2, n2 = n / 2, sq = n2 * n2;
-        Costs r;
-        if (name == "std2") {
-            Costs s = schedule("std2", m2, k2, n2);
-            r.mults = 7 * s.mults;
-            r.adds = 7 * s.adds + 4 * m2 * k2 + 4 * k2 * n2 + 7 * m2 * n2;
-            r.moves = 7 * s.moves;
-            const std::uint64_t w = m2 * std::max(k2, n2) + k2 * n2;
-            r.peak = w + s.peak;
-            r.total = w + 7 * s.total;
-        } else if (name == "acc3") {
-            Costs sa = schedule("acc3", m2, k2, n2), sp = schedule("std2", m2, k2, n2);
-            r.mults = 5 * sa.mults + 2 * sp.mults;
-            r.adds = 5 * sa.adds + 2 * sp.adds + 4 * m2 * k2 + 4 * k2 * n2 + 6 * m2 * n2;
-            r.moves = 5 * sa.moves + 2 * sp.moves;
-            const std::uint64_t w = m2 * k2 + k2 * n2 + m2 * n2;
-            r.peak = w + std::max(sa.peak, sp.peak);
-            r.total = w + 5 * sa.total + 2 * sp.total;
-        } else if (name == "ip") {
-            Costs s = schedule("ip", m2, k2, n2);
-            r.mults = 7 * s.mults;
-            r.adds = 7 * s.adds + 15 * sq;
-        } else if (name == "ovl" || name == "ovr") {
-            Costs s = schedule(name, m2, k2, n2), ipc = schedule("ip", m2, k2, n2);
-            r.mults = 4 * s.mults + 3 * ipc.mults;
-            r.adds = 4 * s.adds + 3 * ipc.adds + 15 * sq;
-            r.peak = sq + std::max(s.peak, ipc.peak);
-            r.total = sq + 4 * s.total;
-        } else if (name == "ovl2") {
-            Costs so = schedule("ovl", m2, k2, n2), sr = schedule("ovr", m2, k2, n2),
-                  ipc = schedule("ip", m2, k2, n2);
-            r.mults = 4 * so.mults + sr.mults + 2 * ipc.mults;
-            r.adds = 4 * so.adds + sr.adds + 2 * ipc.adds + 15 * sq;
-            r.moves = 2 * sq + 4 * so.moves + sr.moves;
-            r.peak = sq + std::max({so.peak, sr.peak, ipc.peak});
-            r.total = sq + 4 * so.total + sr.total;
-        } else if (name == "aclr") {
-            Costs s = schedule("aclr", m2, k2, n2), ipc = schedule("ip", m2, k2, n2);
-            r.mults = 4 * s.mults + 3 * ipc.mults;
-            r.adds = 4 * s.adds + 3 * ipc.adds + 17 * sq;
-            r.peak = 2 * sq + std::max(s.peak, ipc.peak);
-            r.total = 2 * sq + 4 * s.total;
-        } else if (name == "accr") {
-            Costs s = schedule("accr", m2, k2, n2), ovr = schedule("ovr", m2, k2, n2),
-                  ipc = schedule("ip", m2, k2, n2);
-            r.mults = 4 * s.mults + 2 * ovr.mults + ipc.mults;
-            r.adds = 4 * s.adds + 2 * ovr.adds + ipc.adds + 17 * sq;
-            r.peak = 2 * sq + std::max({s.peak, ovr.peak, ipc.peak});
-            r.total = 2 * sq + 4 * s.total + 2 * ovr.total;
-        } else if (name == "acc2") {
-            Costs s = schedule("acc2", m2, k2, n2), w = schedule("std2", m2, k2, n2),
-                  lr = schedule("aclr", m2, k2, n2), rr = schedule("accr", m2, k2, n2);
-            r.mults = 4 * s.mults + w.mults + lr.mults + rr.mults;
-            r.adds = 4 * s.adds + w.adds + lr.adds + rr.adds + 17 * sq;
-            r.peak = 2 * sq + std::max({s.peak, w.peak, lr.peak, rr.peak});
-            r.total = 2 * sq + 4 * s.total + w.total + lr.total + rr.total;
-        } else if (name == "acr") {
-            Costs s = schedule("acr", m2, k2, n2), w = schedule("std2", m2, k2, n2);
-            r.mults = 5 * s.mults + 2 * w.mults;
-            r.adds = 5 * s.adds + 2 * w.adds + 4 * m2 * k2 + 4 * k2 * n2 + 8 * m2 * n2;
-            const std::uint64_t words = std::max(m2, k2) * n2 + m2 * k2;
-            r.peak = words + std::max(s.peak, w.peak);
-            r.total = words + 5 * s.total + 2 * w.total;
-        } else {
-            fail(E_UNKNOWN_SCHEDULE, "expected_costs: unknown variant " + name);
-        }
-        return r;
-    }
-
-    int cutoff_;
-    std::map<std::tuple<std::string, std::uint64_t, std::uint64_t, std::uint64_t>, Costs> memo_;
-};
+// ------------------------------------------------------------ driver helpers
 
 bool parse_blocked(const std::string& v, int* t, std::string* base) {
     const std::string pre = "blocked_acc_t";
@@ -273,53 +158,6 @@ const char* iprect_block_variant(std::uint64_t i, std::uint64_t j, std::uint64_t
     if (last_j) return "ovl";            // A_i's last use
     if (last_i) return "ovr";            // B_j's last use
     return "std2";
-}
-
-}  // namespace
-
-Costs expected_costs(const std::string& variant, std::uint64_t m, std::uint64_t k,
-                     std::uint64_t n, int cutoff) {
-    Evaluator ev(cutoff);
-    int t;
-    std::string base;
-    if (variant == "classic") return classical_costs(m, k, n, false);
-    if (variant == "ipmm") return ev.ipmm(n, k);
-    if (variant == "ipovmm") {
-        const std::uint64_t m0 = m / n, k0 = k / n;
-        Costs w = ev.schedule("std2", n, n, n), o = ev.schedule("ovl", n, n, n),
-              a = ev.schedule("acc3", n, n, n);
-        Costs r;
-        r.mults = w.mults + (m0 - 1) * o.mults + (k0 - 1) * m0 * a.mults;
-        r.adds = w.adds + (m0 - 1) * o.adds + (k0 - 1) * m0 * a.adds;
-        r.moves = (m0 - 1) * o.moves;
-        return r;
-    }
-    if (variant == "iprect") {
-        const std::uint64_t mb = m / k, nb = n / k;
-        Costs r;
-        for (std::uint64_t i = 0; i < mb; ++i)
-            for (std::uint64_t j = 0; j < nb; ++j) {
-                Costs c = ev.schedule(iprect_block_variant(i, j, mb, nb), k, k, k);
-                r.mults += c.mults;
-                r.adds += c.adds;
-                r.moves += c.moves;
-            }
-        return r;
-    }
-    if (parse_blocked(variant, &t, &base)) {
-        const std::uint64_t s = n / static_cast<std::uint64_t>(t);
-        const std::uint64_t chunk = base == "acc2" ? 2 * (s * s - 1) / 3 : s * s;
-        Costs b = ev.schedule(base, s, s, s);
-        const std::uint64_t calls = static_cast<std::uint64_t>(t) * t * t;
-        Costs r;
-        r.mults = calls * b.mults;
-        r.adds = calls * b.adds;
-        r.moves = calls * b.moves;
-        r.peak = chunk;
-        r.total = chunk;
-        return r;
-    }
-    return ev.schedule(variant, m, k, n);
 }
 
 bool variant_accumulates(const std::string& v) {

@@ -108,12 +108,19 @@ Plan plan_variant(const std::string& variant, Field f, std::uint64_t m, std::uin
                   std::uint64_t n, std::uint64_t lda, std::uint64_t ldb, std::uint64_t ldc,
                   Scalar alpha, Scalar beta, int cutoff, const PlanOptions& opt);
 
-// Expected costs (models.hpp:202-229), the planner's own model.
+// Expected costs of a variant (the reference's models.hpp:202-229 answers the
+// same question); wm_costs.cpp derives them from the schedule IR.
 struct Costs {
     std::uint64_t mults = 0, adds = 0, peak = 0, total = 0, moves = 0;
 };
 Costs expected_costs(const std::string& variant, std::uint64_t m, std::uint64_t k,
                      std::uint64_t n, int cutoff);
+
+// "blocked_acc_t<T>[_acc2]" -> T and the base schedule (acc3 / acc2)
+bool parse_blocked(const std::string& variant, int* t, std::string* base);
+// Config-3 composition: the schedule for block (i, j) of an mb x nb grid of squares.
+const char* iprect_block_variant(std::uint64_t i, std::uint64_t j, std::uint64_t mb,
+                                 std::uint64_t nb);
 
 bool variant_accumulates(const std::string& variant);
 Contract variant_contract(const std::string& variant);

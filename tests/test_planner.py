@@ -63,6 +63,32 @@ def test_expected_costs_match_oracle_models(W):
     assert (r.mults, r.adds, r.peak_extra_words) == (e["mults"], e["adds"], 0)
 
 
+def test_expected_costs_match_reference_directly(W, O):
+    """The product's IR-derived cost model (wm_costs.cpp) against the reference's
+    own expected_costs (models.hpp:202-229), squares and rectangles, every
+    builtin and driver."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    fields = ("mults", "adds", "peak_extra_words", "total_alloc_words", "word_moves")
+
+    def same(v, m, k, n, c):
+        r = W.expected_costs(v, m, k, n, c)
+        e = O.ref_expected_costs(v, m, k, n, c)
+        assert tuple(getattr(r, f) for f in fields) == tuple(e[f] for f in fields), (v, m, k, n, c)
+
+    square = ("std2", "acc3", "ip", "ovl", "ovl2", "ovr", "aclr", "accr", "acc2", "acr", "ipmm",
+              "classic", "blocked_acc_t2", "blocked_acc_t4", "blocked_acc_t2_acc2")
+    for v in square:
+        for (n, c) in [(2, 1), (16, 1), (64, 2), (256, 8), (2048, 64), (16384, 512), (32768, 1024)]:
+            same(v, n, n, n, c)
+    for v in ("std2", "acc3", "acr", "classic"):  # rectangular schedules
+        for (m, k, n, c) in [(32, 16, 8, 1), (8, 64, 32, 2), (512, 256, 1024, 16)]:
+            same(v, m, k, n, c)
+    for (m, k, n) in [(8, 8, 2), (64, 32, 16), (1024, 2048, 256)]:
+        same("ipovmm", m, k, n, 1)
+        same("ipovmm", m, k, n, 8)
+
+
 # SURVEY.md Appendix A / B and 8(d): config-level plans
 CONFIGS = [
     # variant, m, k, n, cutoff, beta, peak words, frames, leaves
