@@ -8,10 +8,13 @@ SplitMix64 seeds A=2, B=3, C=4 stored as float64, cutoff 256 (depth 4).
 A step is one full multiplication with the inputs resident in HBM; the
 400 MB of inputs exceed the 126 MB L2, so no flush is needed between steps.
 
-Multi-GPU (torchrun, one process per GPU): the 7 top-level Winograd products of
-ONE multiplication are partitioned over the ranks (paper_0707_2347_b200/dist.py;
-NCCL point-to-point carries operand blocks out and products back), strong
-scaling; ranks are timed on the device and the max over ranks is reported.
+Multi-GPU (one process per GPU; ``--gpus N`` re-executes itself under
+torch.distributed.run when WORLD_SIZE is unset): the 7^L top-level Winograd
+products of ONE multiplication are partitioned over the ranks
+(paper_0707_2347_b200/dist.py: A and B broadcast over NCCL, operands formed on
+the owning rank, products sent back and folded into C on the root), strong
+scaling; ranks are timed on the device and the max over ranks is reported,
+with every rank's peak extra bytes.
 
 ``--impl reference`` times the reference's own CPU implementation (the
 unmodified winomem headers compiled into oracle/_ref) on the host cores.
@@ -155,22 +158,65 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def cpu_reference_rate(cfg, threads, sample_n=None):
-    """Run the reference run_variant (oracle/_ref) on `threads` host threads at
-    once, each on its own copy of the workload (or of a bounded sample).
-    Returns (GFLOP/s aggregate, seconds, sample description)."""
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def tensor_peaks():
+    for rnd in ("r2", "r1"):
+        f = os.path.join(ROOT, "profiles", rnd, "tensor_peaks.json")
+        if os.path.exists(f):
+            return json.load(open(f)), "measured (profiles/%s/tensor_peaks.json)" % rnd
+    return {}, None
+
+
+def relaunch_under_torchrun(args):
+    """--gpus N > 1 outside torchrun: re-exec this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+# the reference's own single-threaded CPU path, one full multiplication per
+# host thread; C4 at full size is ~30 min per thread and runs as its ipmm
+# 4096^3 cutoff-128 proxy (SURVEY.md 8(d)), marked same_config: false
+REF_PROXY = {"C4": (4096, 128)}
+
+
+def cpu_reference_rate(cfg, config, threads):
+    """Run the reference run_variant (oracle/_ref, -O3 -DNDEBUG) on `threads`
+    host threads at once, each on its own copy of the workload.  Returns
+    (GFLOP/s aggregate, seconds, sample description, same_config)."""
     from concurrent.futures import ThreadPoolExecutor
 
     import numpy as np
 
     from oracle import oracle as O
 
-    m, k, n = cfg["m"], cfg["k"], cfg["n"]
-    cutoff = cfg["cutoff"]
-    if sample_n:
-        scale = m // sample_n
-        m, k, n, cutoff = m // scale, k // scale, n // scale, max(1, cutoff // scale)
+    m, k, n, cutoff = cfg["m"], cfg["k"], cfg["n"], cfg["cutoff"]
+    same = True
+    if config in REF_PROXY:
+        m = k = n = REF_PROXY[config][0]
+        cutoff = REF_PROXY[config][1]
+        same = False
     variant = cfg["variant"]
+    # no reference schedule runs the in-place rectangle: its closest path is std2
+    # on the same shape (SURVEY.md 8(d))
     ref_variant = "std2" if variant == "iprect" else variant
     A = O.fill_random(m, k, cfg["seed"])
     B = O.fill_random(k, n, cfg["seed"] + 1)
@@ -183,9 +229,10 @@ def cpu_reference_rate(cfg, threads, sample_n=None):
     with ThreadPoolExecutor(max_workers=threads) as ex:
         list(ex.map(one, range(threads)))
     dt = time.perf_counter() - t0
-    sample = (f"{threads} concurrent reference run_variant('{ref_variant}') calls on "
-              f"{m}x{k}x{n}, cutoff {cutoff} (oracle/_ref, -O3 -DNDEBUG, 1 thread each)")
-    return threads * 2.0 * m * n * k / dt / 1e9, dt, sample
+    sample = (f"{threads} concurrent reference run_variant('{ref_variant}') calls, each the full "
+              f"{m}x{k}x{n} cutoff {cutoff} multiplication (oracle/_ref: the unmodified reference "
+              f"headers at -O3 -DNDEBUG; the reference is single-threaded per multiply)")
+    return threads * 2.0 * m * n * k / dt / 1e9, dt, sample, same
 
 
 def run_reference_arm(args, cfg):
@@ -193,41 +240,145 @@ def run_reference_arm(args, cfg):
     if rank != 0:
         return
     from oracle import oracle as O
-    if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
-        return
-    threads = os.cpu_count() or 1
-    # bounded sample: the full problem when the whole run fits in ~3 minutes
-    full_est = {"C1": 0.3, "C2": 20.0, "C3": 60.0, "C4": 1800.0, "C5": 1e9}[args.config]
-    total_steps = args.steps + min(args.warmup, 1)
-    sample_n = None
     if cfg["field"] == "real":
         print(json.dumps({"impl": "reference",
                           "unavailable": "no reference float64 path (SPEC.md:94)"}))
         return
-    if full_est * total_steps > 180:
-        sample_n = 2048 if args.config in ("C2", "C3") else 1024
-    for _ in range(min(args.warmup, 1)):
-        cpu_reference_rate(cfg, threads, sample_n)
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, args.config, threads)
     rates, secs = [], []
-    sample = ""
+    sample, same = "", True
     for _ in range(args.steps):
-        r, dt, sample = cpu_reference_rate(cfg, threads, sample_n)
+        r, dt, sample, same = cpu_reference_rate(cfg, args.config, threads)
         rates.append(r)
         secs.append(dt)
     value = statistics.median(rates)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s",
-        "n_gpus": world, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "n_gpus": max(world, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * statistics.median(secs), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (SplitMix64 seeds, residues mod 65521)",
-        "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"]},
+        "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
+                   "same_config": same},
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads,
-                         "kind": "reference", "sample": sample},
+                         "kind": "reference", "sample": sample, "host": host_info()},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }))
+
+
+def measure_rooflines(ctx, step, rep, real, config):
+    """Replay the step with only one kernel class (measurement-only `subset`
+    option) and report each class's algorithmic bytes (or limb ops) over its
+    measured time.  The headline class is the one with the largest share of the
+    step in the committed ncu launch list (scripts/ncu_launch_summary.py), else
+    the longest replay; the frame GEMM's tensor fraction always rides along."""
+    import torch
+
+    stream = ctx.stream
+
+    def subset_time(sub, reps=3):
+        ctx.set_option("subset", sub)
+        step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ctx.enter()
+        e0.record(stream)
+        for _ in range(reps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ctx.set_option("subset", 0)
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    t_add = subset_time(1)
+    t_leaf = subset_time(2)
+    t_frame = subset_time(3) if rep.fused_frames else 0.0
+    parts = ({"prep": subset_time(4), "gemm": subset_time(5), "comb": subset_time(6)}
+             if rep.fused_frames else {})
+    hbm, hbm_src = peaks()
+    tpk, tpk_src = tensor_peaks()
+    rooflines = {
+        "additions": {"bound": "hbm", "kernel": "k_group / k_addsub (block additions)",
+                      "algorithmic_bytes_per_step": rep.add_bytes_issued, "seconds_per_step": t_add},
+        "frame_prep": {"bound": "hbm", "kernel": "k_frame_prep_limbs (S/T + raw limb planes)",
+                       "algorithmic_bytes_per_step": rep.frame_prep_bytes,
+                       "seconds_per_step": parts.get("prep", 0.0)},
+        "frame_gemm": {"bound": "tensor", "kernel": "k_gemm_direct (7 leaf products per launch, "
+                                                    "tcgen05 kind::i8 on 2 x u8 limbs)",
+                       "algorithmic_bytes_per_step": rep.frame_gemm_bytes,
+                       "seconds_per_step": parts.get("gemm", 0.0),
+                       "algorithmic_ops_per_step": 4 * rep.frame_leaf_flops},
+        "frame_comb": {"bound": "hbm", "kernel": "k_frame_comb (U-chain, alpha/beta)",
+                       "algorithmic_bytes_per_step": rep.frame_comb_bytes,
+                       "seconds_per_step": parts.get("comb", 0.0)},
+        "leaf_products": {"bound": "tensor",
+                          "kernel": ("k_leaf_dmma (float64 DMMA leaves)" if real else
+                                     "k_gemm_tma / k_gemm_i8 (unfused int8-limb leaves)"),
+                          "algorithmic_bytes_per_step": None, "seconds_per_step": t_leaf,
+                          "algorithmic_ops_per_step": (rep.leaf_flops - rep.frame_leaf_flops) *
+                                                      (1 if real else 4)},
+        "fused_frames": {"bound": "hbm",
+                         "kernel": "fused leaf frames (prep + GEMM + comb, three launches)",
+                         "algorithmic_bytes_per_step": rep.frame_bytes,
+                         "seconds_per_step": t_frame},
+    }
+    for name, r_ in rooflines.items():
+        b, t = r_["algorithmic_bytes_per_step"], r_["seconds_per_step"]
+        if r_["bound"] == "tensor":
+            # float64: 2mnk DMMA flops vs measured cuBLAS DGEMM; mod p: 4 x 2mnk
+            # int8 limb ops vs measured cuBLASLt int8 (burst, clock-recorded)
+            ops = r_["algorithmic_ops_per_step"]
+            pk = tpk.get("fp64_tflops" if real else "int8_tops")
+            if b and t:  # the operand / product plane stream it also moves
+                r_["achieved_bytes_gbs"] = b / t / 1e9
+            r_["achieved"] = ops / t / 1e12 if t and ops else None
+            r_["peak"] = pk
+            r_["unit"] = "TFLOP/s" if real else "TOP/s"
+            r_["peak_source"] = tpk_src if pk else None
+            r_["frac"] = r_["achieved"] / pk if r_["achieved"] and pk else None
+            continue
+        r_["achieved"] = b / t / 1e9 if b and t else None
+        r_["peak"] = hbm
+        r_["unit"] = "GB/s"
+        r_["peak_source"] = hbm_src
+        r_["frac"] = r_["achieved"] / hbm if r_["achieved"] else None
+    single = [k_ for k_ in rooflines if k_ != "fused_frames" and rooflines[k_]["seconds_per_step"]]
+    share, traffic_cls, basis = None, {}, "longest subset replay"
+    for rnd in ("r2", "r1"):
+        tfile = os.path.join(ROOT, "profiles", rnd, "ncu_launch_summary_%s.json" % config.lower())
+        if os.path.exists(tfile):
+            classes = json.load(open(tfile)).get("classes", {})
+            share = {k_: v["share_of_step"] for k_, v in classes.items() if k_ in single}
+            traffic_cls = classes
+            basis = "largest share of the step in the ncu launch list (profiles/%s)" % rnd
+            break
+    if share:
+        dominant = max(share, key=share.get)
+    else:
+        dominant = max(single, key=lambda k_: rooflines[k_]["seconds_per_step"])
+    dom = rooflines[dominant]
+    cls = traffic_cls.get(dominant)
+    roof = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
+            "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"],
+            "traffic": cls.get("dram_bytes_per_step") if cls else None,
+            "traffic_unit": "dram bytes per step (class total, ncu capture)",
+            "peak_source": dom.get("peak_source"), "class": dominant, "class_basis": basis,
+            "ncu_share_of_step": share,
+            "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
+            "algorithmic_ops_per_step": dom.get("algorithmic_ops_per_step"),
+            "kernel_seconds_per_step": dom["seconds_per_step"]}
+    g = rooflines["frame_gemm"] if rep.fused_frames else rooflines["leaf_products"]
+    roof["tensor_class"] = {k_: g.get(k_) for k_ in ("kernel", "achieved", "peak", "unit", "frac",
+                                                     "peak_source", "seconds_per_step")}
+    return rooflines, roof, {"additions": t_add, "leaf_products": t_leaf,
+                             "fused_frames": t_frame}, parts
 
 
 def main():
@@ -247,16 +398,24 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, cfg)
         return
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if os.environ.get("WM_BENCH_RANKS_ONLY"):  # launcher check (tests/test_bench_cli.py)
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local}), flush=True)
+        return
 
     import numpy as np
     import torch
 
     import paper_0707_2347_b200 as W
 
-    rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         run_partitioned(args, cfg, rank, world, local)
         dist.destroy_process_group()
@@ -270,10 +429,6 @@ def main():
     ctx.set_option("leaf_kernel", args.leaf)
     ctx.set_option("fuse_frames", args.fuse)
     ctx.set_option("graphs", 1)
-    if os.environ.get("WM_FRAME_CFG"):
-        ctx.set_option("frame_cfg", int(os.environ["WM_FRAME_CFG"]))
-    if os.environ.get("WM_GEMM_ENGINE"):
-        ctx.set_option("gemm_engine", int(os.environ["WM_GEMM_ENGINE"]))
     for kv in filter(None, os.environ.get("WM_OPTS", "").split(",")):  # measurement sweeps
         opt_name, opt_val = kv.split("=")
         ctx.set_option(opt_name.strip(), int(opt_val))
@@ -294,29 +449,13 @@ def main():
     reset_inputs()
     rep = step()
     torch.cuda.synchronize()
-    parity = None
     if not real:
         gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_hashes.json")))
         h = "%016x" % C.hash()
         want = gold.get(args.config, {}).get("appendix_a")
         parity = {"c_hash": h, "golden": want, "ok": h == want}
     else:
-        # float64: ||C - AB||_F / ||AB||_F estimated with Gaussian
-        # probe vectors (E ||dC x||^2 = ||dC||_F^2), the classical product applied
-        # as A (B x) in float64; stated tolerance 1e-12 * 2^depth
-        g = torch.Generator(device=C.t.device).manual_seed(1234)
-        num = den = 0.0
-        for _ in range(4):
-            x = torch.randn(n, 1, dtype=torch.float64, device=C.t.device, generator=g)
-            ref = A.t @ (B.t @ x)
-            num += float(((C.t @ x) - ref).square().sum())
-            den += float(ref.square().sum())
-        depth = 0
-        while (max(m, k, n) >> depth) > cfg["cutoff"]:
-            depth += 1
-        err = (num / den) ** 0.5
-        parity = {"rel_frobenius_estimate": err, "probes": 4, "depth": depth,
-                  "tolerance": 1e-12 * 2 ** depth, "ok": err <= 1e-12 * 2 ** depth}
+        parity = real_parity(A, B, C, m, k, n, cfg)
 
     in_place = cfg["variant"] in ("iprect",)
     for _ in range(args.warmup):
@@ -324,8 +463,6 @@ def main():
             reset_inputs()
         step()
     torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
     stream = ctx.stream
     small = 8 * (m * k + k * n + m * n) <= 126e6
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}") \
@@ -347,106 +484,10 @@ def main():
         torch.cuda.synchronize()
     times = [a.elapsed_time(b) / 1e3 for a, b in evs]
     t_step = sum(times) / len(times)
-    if world > 1:
-        t = torch.tensor([t_step], device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_step = float(t.item())
     flops = 2.0 * m * n * k
-    value = world * flops / t_step / 1e9
+    value = flops / t_step / 1e9
 
-    # attribution: additions-only and leaves/frames-only replays (measurement only)
-    def subset_time(sub, reps=3):
-        ctx.set_option("subset", sub)
-        step()
-        torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        ctx.enter()
-        e0.record(stream)
-        for _ in range(reps):
-            step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ctx.set_option("subset", 0)
-        return e0.elapsed_time(e1) / 1e3 / reps
-
-    t_add = subset_time(1)
-    t_leaf = subset_time(2)
-    t_frame = subset_time(3) if rep.fused_frames else 0.0
-    frame_parts = ({"prep": subset_time(4), "gemm": subset_time(5), "comb": subset_time(6)}
-                   if rep.fused_frames else {})
-
-    hbm, hbm_src = peaks()
-    comps = {"additions": t_add, "leaf_products": t_leaf, "fused_frames": t_frame}
-    # every kernel is bound by HBM / L2 bytes at these sizes (the int8 tensor
-    # work is 4 x 2mnk limb ops against >= 4 POPS): bytes over measured time.
-    # Single-kernel classes compete for "dominant"; fused_frames is the sum of
-    # its three kernels and is reported beside them.
-    rooflines = {
-        "additions": {"bound": "hbm", "kernel": "k_group / k_addsub (block additions)",
-                      "algorithmic_bytes_per_step": rep.add_bytes_issued, "seconds_per_step": t_add},
-        "frame_prep": {"bound": "hbm", "kernel": "k_frame_prep_limbs (S/T + raw limb planes)",
-                       "algorithmic_bytes_per_step": rep.frame_prep_bytes,
-                       "seconds_per_step": frame_parts.get("prep", 0.0)},
-        "frame_gemm": {"bound": "tensor", "kernel": "k_gemm_direct (7 leaf products per launch, "
-                                                    "tcgen05 kind::i8 on 2 x u8 limbs)",
-                       "algorithmic_bytes_per_step": rep.frame_gemm_bytes,
-                       "seconds_per_step": frame_parts.get("gemm", 0.0),
-                       "algorithmic_ops_per_step": 4 * rep.frame_leaf_flops},
-        "frame_comb": {"bound": "hbm", "kernel": "k_frame_comb (U-chain, alpha/beta)",
-                       "algorithmic_bytes_per_step": rep.frame_comb_bytes,
-                       "seconds_per_step": frame_parts.get("comb", 0.0)},
-        "leaf_products": {"bound": "tensor",
-                          "kernel": ("k_leaf_dmma (float64 DMMA leaves)" if real else
-                                     "k_gemm_tma / k_gemm_i8 (unfused int8-limb leaves)"),
-                          "algorithmic_bytes_per_step": None, "seconds_per_step": t_leaf,
-                          "algorithmic_ops_per_step": (rep.leaf_flops - rep.frame_leaf_flops) *
-                                                      (1 if real else 4)},
-        "fused_frames": {"bound": "hbm",
-                         "kernel": "fused leaf frames (prep + GEMM + comb, three launches)",
-                         "algorithmic_bytes_per_step": rep.frame_bytes,
-                         "seconds_per_step": t_frame},
-    }
-    tpk_file = os.path.join(ROOT, "profiles", "r1", "tensor_peaks.json")
-    tpk = json.load(open(tpk_file)) if os.path.exists(tpk_file) else {}
-    for name, r_ in rooflines.items():
-        b, t = r_["algorithmic_bytes_per_step"], r_["seconds_per_step"]
-        if r_["bound"] == "tensor":
-            # float64: 2mnk DMMA flops vs measured cuBLAS DGEMM; mod p: 4 x 2mnk
-            # int8 limb ops vs measured cuBLASLt int8
-            ops = r_["algorithmic_ops_per_step"]
-            pk = tpk.get("fp64_tflops" if real else "int8_tops")
-            if b and t:  # the operand / product plane stream it also moves
-                r_["achieved_bytes_gbs"] = b / t / 1e9
-            r_["achieved"] = ops / t / 1e12 if t and ops else None
-            r_["peak"] = pk
-            r_["unit"] = "TFLOP/s" if real else "TOP/s"
-            r_["peak_source"] = ("measured (profiles/r1/tensor_peaks.json)" if pk else None)
-            r_["frac"] = r_["achieved"] / pk if r_["achieved"] and pk else None
-            continue
-        r_["achieved"] = b / t / 1e9 if b and t else None
-        r_["peak"] = hbm
-        r_["unit"] = "GB/s"
-        r_["frac"] = r_["achieved"] / hbm if r_["achieved"] else None
-    single = [k_ for k_ in rooflines if k_ != "fused_frames"]
-    dominant = max(single, key=lambda k_: rooflines[k_]["seconds_per_step"] or 0.0)
-    dom = rooflines[dominant]
-    traffic = None
-    # dram read + write bytes of the class per step, summed over its launches in the
-    # committed ncu launch list (scripts/ncu_launch_summary.py; ncu replays each
-    # launch serialised with a cold cache)
-    tfile = os.path.join(ROOT, "profiles", "r1", "ncu_launch_summary_%s.json" % args.config.lower())
-    if os.path.exists(tfile):
-        cls = json.load(open(tfile)).get("classes", {}).get(dominant)
-        traffic = cls.get("dram_bytes_per_step") if cls else None
-    roof = {"bound": dom["bound"], "kernel": dom["kernel"], "achieved": dom["achieved"],
-            "peak": dom["peak"], "unit": dom["unit"], "frac": dom["frac"], "traffic": traffic,
-            "traffic_unit": "dram bytes per step (class total, ncu capture)",
-            "peak_source": dom.get("peak_source") or hbm_src, "class": dominant,
-            "algorithmic_bytes_per_step": dom["algorithmic_bytes_per_step"],
-            "algorithmic_ops_per_step": dom.get("algorithmic_ops_per_step"),
-            "kernel_seconds_per_step": dom["seconds_per_step"]}
-
+    rooflines, roof, comps, frame_parts = measure_rooflines(ctx, step, rep, real, args.config)
     out = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
@@ -457,7 +498,7 @@ def main():
             "uniform[-1,1)" if real else "residues mod 65521"),
         "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
                    "m": m, "k": k, "n": n, "cutoff": cfg["cutoff"], "alpha": cfg["alpha"],
-                   "beta": cfg["beta"], "parallelism": "replicas" if world > 1 else "single",
+                   "beta": cfg["beta"], "parallelism": "single",
                    "l2": "inputs (%.0f MB) %s L2; %s" % (
                        8 * (m * k + k * n + m * n) / 1e6,
                        ">" if 8 * (m * k + k * n + m * n) > 126e6 else "<=",
@@ -477,28 +518,45 @@ def main():
         "launches_per_step": rep.n_launches,
         "clocks": clk.summary(),
     }
-
-    if rank == 0 and world == 1 and not args.no_e2e and not real:
+    if not args.no_e2e and not real:
         out["e2e"] = e2e(W, cfg, args, np, torch)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not real:
+    if not args.no_cpu_baseline and not real:
         try:
-            r, dt, sample = cpu_reference_rate(cfg, 1, None if args.config in ("C1", "C2")
-                                               else 2048)
+            r, dt, sample, same = cpu_reference_rate(cfg, args.config, 1)
             out["cpu_baseline"] = {"value": r, "unit": "GFLOP/s", "cores": 1,
-                                   "kind": "reference", "sample": sample,
-                                   "seconds": dt}
+                                   "kind": "reference", "sample": sample, "same_config": same,
+                                   "seconds": dt, "host": host_info()}
         except Exception as e:  # pragma: no cover
             out["cpu_baseline"] = {"value": None, "error": str(e)}
-    if rank == 0:
-        print(json.dumps(out))
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    print(json.dumps(out))
+
+
+def real_parity(A, B, C, m, k, n, cfg):
+    """float64: ||C - AB||_F / ||AB||_F estimated with Gaussian probe
+    vectors (E ||dC x||^2 = ||dC||_F^2), the classical product applied as A (B x)
+    in float64; stated tolerance 1e-12 * 2^depth."""
+    import torch
+    g = torch.Generator(device=C.t.device).manual_seed(1234)
+    num = den = 0.0
+    for _ in range(4):
+        x = torch.randn(n, 1, dtype=torch.float64, device=C.t.device, generator=g)
+        ref = A.t @ (B.t @ x)
+        num += float(((C.t @ x) - ref).square().sum())
+        den += float(ref.square().sum())
+    depth = 0
+    while (max(m, k, n) >> depth) > cfg["cutoff"]:
+        depth += 1
+    err = (num / den) ** 0.5
+    return {"rel_frobenius_estimate": err, "probes": 4, "depth": depth,
+            "tolerance": 1e-12 * 2 ** depth, "ok": err <= 1e-12 * 2 ** depth}
 
 
 def run_partitioned(args, cfg, rank, world, local):
-    """N > 1: the 7 top-level Winograd products of ONE multiplication are spread
-    over the ranks (paper_0707_2347_b200/dist.py; NCCL point-to-point carries
-    operand blocks out and products back); strong scaling, max over ranks."""
+    """N > 1: the 7^L top-level Winograd products of ONE multiplication are
+    spread over the ranks (paper_0707_2347_b200/dist.py: A and B broadcast,
+    operands formed on the owning rank, products sent back and folded into C on
+    the root); strong scaling, device-timed, max over ranks."""
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -508,53 +566,106 @@ def run_partitioned(args, cfg, rank, world, local):
 
     real = cfg["field"] == "real"
     m, k, n = cfg["m"], cfg["k"], cfg["n"]
-    levels = choose_levels(world)
+    levels = choose_levels(world, min(m, k, n), cfg["cutoff"])
     f = 2 ** levels
     lv = local_variant(cfg["variant"], m // f, k // f, n // f)
     be = CudaBackend(65521, lv, cfg["cutoff"], local, real=real)
-    dev = f"cuda:{local}"
     A = B = C = None
     if rank == 0:
         Am, Bm, Cm = (W.Matrix(m, k, device=local, real=real), W.Matrix(k, n, device=local, real=real),
                       W.Matrix(m, n, device=local, real=real))
-        Am.fill_random(cfg["seed"])
-        Bm.fill_random(cfg["seed"] + 1)
-        if cfg["beta"]:
-            Cm.fill_random(cfg["seed"] + 2)
+
+        def reset():
+            Am.fill_random(cfg["seed"])
+            Bm.fill_random(cfg["seed"] + 1)
+            if cfg["beta"]:
+                Cm.fill_random(cfg["seed"] + 2)
+            else:
+                Cm.fill_zero()
+        reset()
         A, B, C = Am.t, Bm.t, Cm.t
-    ctxs = W.Context.get(local, 65521, real)
 
     def step():
-        partitioned_multiply(A, B, C, cfg["alpha"], cfg["beta"], be, levels=levels)
+        return partitioned_multiply(A, B, C, cfg["alpha"], cfg["beta"], be, levels=levels)
 
     parity = None
-    step()
+    st = step()
     torch.cuda.synchronize()
-    if rank == 0 and not real:
-        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_hashes.json")))
-        h = "%016x" % Cm.hash()
-        want = gold.get(args.config, {}).get("appendix_a")
-        parity = {"c_hash": h, "golden": want, "ok": h == want}
-        if cfg["beta"]:
-            Cm.fill_random(cfg["seed"] + 2)
+    if rank == 0:
+        if real:
+            parity = real_parity(Am, Bm, Cm, m, k, n, cfg)
+        else:
+            gold = json.load(open(os.path.join(ROOT, "tests", "golden", "config_hashes.json")))
+            h = "%016x" % Cm.hash()
+            want = gold.get(args.config, {}).get("appendix_a")
+            parity = {"c_hash": h, "golden": want, "ok": h == want}
+        reset()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
+    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
         e0.record()
         for _ in range(args.steps):
-            step()
+            st = step()
         e1.record()
         torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=dev)
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_step = float(t.item())
+
+    # end to end: pinned host buffers in, C out, on the root, every step
+    e2e_t = None
+    h2d = 8 * (m * k + k * n + (m * n if cfg["beta"] else 0))
     if rank == 0:
-        print(json.dumps({
+        hA = A.to("cpu").pin_memory()
+        hB = B.to("cpu").pin_memory()
+        hC = C.to("cpu").pin_memory()
+    dist.barrier()
+    ts = []
+    for _ in range(max(2, min(args.steps, 5))):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        if rank == 0:
+            A.copy_(hA, non_blocking=True)
+            B.copy_(hB, non_blocking=True)
+            if cfg["beta"]:
+                C.copy_(hC, non_blocking=True)
+        step()
+        if rank == 0:
+            hC.copy_(C, non_blocking=True)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    tt = torch.tensor([statistics.median(ts)], device=f"cuda:{local}")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_t = float(tt.item())
+
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, {"rank": rank, "products": len(st.products),
+                                      "peak_extra_bytes": st.peak_extra_bytes,
+                                      "bytes_sent": st.bytes_sent,
+                                      "bytes_received": st.bytes_received})
+    out = None
+    if rank == 0:
+        # roofline of the per-rank work: one local product replayed by kernel class
+        X = W.Matrix(m // f, k // f, device=local, real=real)
+        Y = W.Matrix(k // f, n // f, device=local, real=real)
+        P = W.Matrix(m // f, n // f, device=local, real=real)
+        X.fill_random(11)
+        Y.fill_random(12)
+        ctx = X.ctx()
+
+        def local_step():
+            return W.run_variant(lv, X, Y, P, alpha=1, beta=0, cutoff=cfg["cutoff"])
+        rep = local_step()
+        rooflines, roof, comps, parts = measure_rooflines(ctx, local_step, rep, real,
+                                                          args.config + "_local")
+        out = {
             "metric": METRIC, "value": 2.0 * m * n * k / t_step / 1e9, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -564,10 +675,21 @@ def run_partitioned(args, cfg, rank, world, local):
             "config": {"workload": args.config + ": " + cfg["desc"], "variant": cfg["variant"],
                        "m": m, "k": k, "n": n, "cutoff": cfg["cutoff"],
                        "parallelism": f"{7 ** levels}-way product partition ({levels} Winograd "
-                                      f"level(s)) over {world} GPUs (NCCL p2p), local schedule {lv}",
+                                      f"level(s)) over {world} GPUs: A/B broadcast, operands "
+                                      f"formed per rank, P_t sent to the root (NCCL); local "
+                                      f"schedule {lv}",
                        "makespan_bound": makespan_bound(world, 7 ** levels)},
             "parity": parity, "clocks": clk.summary(),
-        }))
+            "per_rank": per_rank,
+            "peak_extra_bytes_max_rank": max(r["peak_extra_bytes"] for r in per_rank),
+            "roofline": roof, "rooflines": rooflines,
+            "gpu_launches": None,
+            "e2e": {"value": 2.0 * m * n * k / e2e_t / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * m * n,
+                    "seconds_per_step": e2e_t,
+                    "timing": "host wall clock, pinned float64 buffers on the root, max over ranks"},
+        }
+        print(json.dumps(out))
 
 
 def e2e(W, cfg, args, np, torch):

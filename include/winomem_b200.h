@@ -130,6 +130,11 @@ int wm_block_scale_copy(wm_ctx* ctx, wm_dmat dst, wm_dmat src, uint32_t s);
 /* C <- alpha*A*B + beta*C, C disjoint from A and B (classical_mul, ring.hpp:315-384) */
 int wm_classical_mul(wm_ctx* ctx, wm_dmat C, wm_dmat A, wm_dmat B, uint32_t alpha, uint32_t beta);
 
+/* dst <- sum_{t<n} coef[t]*src[t], 1 <= n <= 4, one pass; dst may alias a source
+ * exactly (new: the S_i / T_i operands and P_i folds of the multi-GPU
+ * partition, dist.py; REAL64 reads each coef as a signed int32) */
+int wm_lincomb(wm_ctx* ctx, wm_dmat dst, int n, const wm_dmat* src, const uint32_t* coef);
+
 /* ---- drivers -------------------------------------------------------------- */
 /* run_variant (drivers.hpp:213-222) / multiply (executor.hpp:240-299):
  * variant is a builtin schedule name (std2 acc3 ip ovl ovl2 ovr aclr accr acc2 acr),
@@ -193,6 +198,9 @@ int wm_run_parsed_schedule_host_u32(wm_ctx* ctx, const char* text, uint64_t m, u
                                     uint32_t alpha, uint32_t beta, int cutoff, wm_report* report);
 
 /* ---- boundary formats ------------------------------------------------------ */
+/* device float64 buffers for staging host views (the C++ drop-in's primitives) */
+int wm_dev_alloc(wm_ctx* ctx, uint64_t words, double** out);
+void wm_dev_free(double* p);
 int wm_upload_u32(wm_ctx* ctx, wm_dmat dst, const uint32_t* host, uint64_t host_ld);
 int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src);
 /* FNV-1a over uint32 residues, row-major (fnv1a64 / Matrix::hash, ring.hpp:107-114,208) */

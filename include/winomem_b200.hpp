@@ -12,6 +12,8 @@
 // device the calls throw.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -122,6 +124,11 @@ class Modulus {
     }
     std::uint32_t p() const { return p_; }
     Elem minus_one() const { return p_ - 1; }
+    Elem reduce_u64(std::uint64_t x) const { return static_cast<Elem>(x % p_); }
+    Elem reduce_i64(std::int64_t x) const {
+        const std::int64_t r = x % static_cast<std::int64_t>(p_);
+        return static_cast<Elem>(r < 0 ? r + p_ : r);
+    }
     Elem add(Elem a, Elem b) const { std::uint32_t s = a + b; return s >= p_ ? s - p_ : s; }
     Elem sub(Elem a, Elem b) const { return a >= b ? a - b : a + p_ - b; }
     Elem neg(Elem a) const { return a ? p_ - a : 0; }
@@ -161,17 +168,53 @@ inline std::uint64_t fnv1a64(const Elem* data, std::size_t count) {
     return wm_fnv1a64_u32(data, count);
 }
 
+// Non-owning window {ptr, rows, cols, stride, origin} into a row-major host
+// buffer (ring.hpp:122-177); `origin` names the owning buffer.
 struct MatView {
     Elem* ptr = nullptr;
     std::size_t rows = 0, cols = 0, stride = 0;
     const Elem* origin = nullptr;
     Elem& at(std::size_t i, std::size_t j) const { return ptr[i * stride + j]; }
+    bool empty() const { return rows == 0 || cols == 0; }
     std::size_t words() const { return rows * cols; }
     MatView window(std::size_t r0, std::size_t c0, std::size_t r, std::size_t c) const {
         if (r0 + r > rows || c0 + c > cols) throw dimension_error("window exceeds view bounds");
         return MatView{ptr + r0 * stride + c0, r, c, stride, origin};
     }
+    bool same_window(const MatView& o) const {
+        return ptr == o.ptr && rows == o.rows && cols == o.cols && stride == o.stride;
+    }
+    std::size_t first_word() const { return static_cast<std::size_t>(ptr - origin); }
+    std::size_t last_word() const { return first_word() + (rows - 1) * stride + cols - 1; }
+    // Do the two windows share an element?  Same buffer and stride: row i of
+    // this and row j of o meet iff (i - j) * stride falls strictly inside
+    // (d - cols, d + o.cols), d = o.ptr - ptr; the admissible t = i - j form an
+    // integer interval, intersected with (-o.rows, rows).  Other strides: word
+    // spans (only provably disjoint temporaries have them).
+    bool overlaps(const MatView& o) const {
+        if (empty() || o.empty() || origin != o.origin) return false;
+        if (stride != o.stride) return first_word() <= o.last_word() && o.first_word() <= last_word();
+        const std::int64_t s = static_cast<std::int64_t>(stride);
+        const std::int64_t d = static_cast<std::int64_t>(o.ptr - ptr);
+        const std::int64_t lo = d - static_cast<std::int64_t>(cols) + 1;   // t*s >= lo
+        const std::int64_t hi = d + static_cast<std::int64_t>(o.cols) - 1; // t*s <= hi
+        auto floor_div = [](std::int64_t a, std::int64_t b) {
+            return a / b - ((a % b != 0) && ((a < 0) != (b < 0)));
+        };
+        const std::int64_t tmin = std::max(-floor_div(-lo, s), 1 - static_cast<std::int64_t>(o.rows));
+        const std::int64_t tmax = std::min(floor_div(hi, s), static_cast<std::int64_t>(rows) - 1);
+        return tmin <= tmax;
+    }
+    bool disjoint(const MatView& o) const { return !overlaps(o); }
 };
+
+// quad_split (ring.hpp:222-228): the four half-size windows, no data moves
+inline std::array<MatView, 4> quad_split(const MatView& v) {
+    if (v.rows % 2 || v.cols % 2) throw odd_dimension_error("quad_split requires even dimensions");
+    const std::size_t r = v.rows / 2, c = v.cols / 2;
+    return {v.window(0, 0, r, c), v.window(0, c, r, c), v.window(r, 0, r, c),
+            v.window(r, c, r, c)};
+}
 
 class Matrix {
   public:
@@ -205,14 +248,132 @@ class Matrix {
 };
 
 // ---- meter (meter.hpp) -----------------------------------------------------
+struct AllocEvent {
+    std::uint64_t words = 0;
+    int depth = 0;
+    std::string slot;
+};
+
 class CostMeter {
   public:
     std::uint64_t mults = 0, adds = 0, word_moves = 0;
     std::uint64_t live_extra_words = 0, peak_extra_words = 0, total_alloc_words = 0;
     std::uint64_t classical_calls = 0;
+    std::vector<AllocEvent> alloc_log;  // every temporary the schedule acquired
     std::map<std::string, std::uint64_t> schedule_calls;
     // device figures of the last call
     std::uint64_t peak_extra_bytes = 0, launches = 0;
+
+    void count_mults(std::uint64_t n) { mults += n; }
+    void count_adds(std::uint64_t n) { adds += n; }
+    void count_moves(std::uint64_t n) { word_moves += n; }
+    void on_alloc(std::uint64_t words, int depth, const std::string& slot) {
+        live_extra_words += words;
+        peak_extra_words = std::max(peak_extra_words, live_extra_words);
+        total_alloc_words += words;
+        alloc_log.push_back({words, depth, slot});
+    }
+    void on_free(std::uint64_t words) { live_extra_words -= words; }
+    void on_classical() { ++classical_calls; }
+    void on_schedule(const std::string& name) { ++schedule_calls[name]; }
+};
+
+// ---- workspaces (workspace.hpp:24-147) --------------------------------------
+// The host-side scratch providers of the reference interface.  The device
+// multiply plans its own HBM arena (the same LIFO frames, reported through
+// CostMeter); these serve host code written against the Workspace plug-in.
+class Workspace {
+  public:
+    virtual ~Workspace() = default;
+    virtual void push_frame() = 0;
+    virtual MatView acquire(std::size_t rows, std::size_t cols, int depth, const char* slot) = 0;
+    virtual void pop_frame() = 0;
+};
+
+class HeapWorkspace : public Workspace {
+  public:
+    explicit HeapWorkspace(CostMeter* meter) : meter_(meter) {}
+    void push_frame() override { frames_.emplace_back(); }
+    MatView acquire(std::size_t rows, std::size_t cols, int depth, const char* slot) override {
+        if (frames_.empty()) throw workspace_error("acquire outside a frame");
+        frames_.back().emplace_back(rows * cols, 0);
+        Elem* p = frames_.back().back().data();
+        if (meter_) meter_->on_alloc(rows * cols, depth, slot ? slot : "");
+        return MatView{p, rows, cols, cols, p};
+    }
+    void pop_frame() override {
+        if (frames_.empty()) throw workspace_error("pop without frame");
+        if (meter_)
+            for (const auto& b : frames_.back()) meter_->on_free(b.size());
+        frames_.pop_back();
+    }
+
+  private:
+    CostMeter* meter_;
+    std::vector<std::vector<std::vector<Elem>>> frames_;
+};
+
+class BumpWorkspace : public Workspace {
+  public:
+    BumpWorkspace(Elem* base, std::size_t words) : base_(base), cap_(words) {}
+    void push_frame() override { marks_.push_back(used_); }
+    MatView acquire(std::size_t rows, std::size_t cols, int, const char*) override {
+        if (marks_.empty()) throw workspace_error("acquire outside a frame");
+        const std::size_t need = rows * cols;
+        if (need > cap_ - used_)
+            throw workspace_error("scratch chunk exhausted: need " + std::to_string(need) +
+                                  " words, free " + std::to_string(cap_ - used_));
+        Elem* p = base_ + used_;
+        used_ += need;
+        high_ = std::max(high_, used_);
+        return MatView{p, rows, cols, cols, base_};
+    }
+    void pop_frame() override {
+        if (marks_.empty()) throw workspace_error("pop without frame");
+        used_ = marks_.back();
+        marks_.pop_back();
+    }
+    std::size_t high_water() const { return high_; }
+
+  private:
+    Elem* base_;
+    std::size_t cap_, used_ = 0, high_ = 0;
+    std::vector<std::size_t> marks_;
+};
+
+class QuadrantWorkspace : public Workspace {
+  public:
+    explicit QuadrantWorkspace(MatView donor) {
+        if (donor.rows != donor.cols) throw workspace_error("quadrant workspace donor must be square");
+        regions_.push_back({donor, 0});
+    }
+    void push_frame() override {
+        Region next = {regions_.back().view, 0};
+        if (regions_.back().taken) {  // descend into the free fourth quadrant
+            if (next.view.rows < 2) throw workspace_error("scratch region exhausted");
+            next.view = quad_split(next.view)[3];
+        }
+        regions_.push_back(next);
+    }
+    MatView acquire(std::size_t rows, std::size_t cols, int, const char* slot) override {
+        Region& r = regions_.back();
+        if (r.view.rows < 2 || rows > r.view.rows / 2 || cols > r.view.cols / 2)
+            throw workspace_error(std::string("temporary ") + (slot ? slot : "") +
+                                  " does not fit the scratch region");
+        if (r.taken == 3) throw workspace_error("more than three temporaries in a frame");
+        return quad_split(r.view)[r.taken++].window(0, 0, rows, cols);
+    }
+    void pop_frame() override {
+        if (regions_.size() < 2) throw workspace_error("pop without frame");
+        regions_.pop_back();
+    }
+
+  private:
+    struct Region {
+        MatView view;
+        int taken;
+    };
+    std::vector<Region> regions_;
 };
 
 struct CostReport {
@@ -334,14 +495,148 @@ inline void classical_mul(Matrix& C, Matrix& A, Matrix& B, Elem alpha, Elem beta
     run_variant("classic", A, B, C, {alpha, beta, 1});
 }
 
+// ---- the primitive operators on host views (ring.hpp:241-384) ---------------
+// Each call checks the reference's aliasing rules on the host views, stages the
+// windows on the device (one strided copy each; a window that exactly aliases
+// another shares its device copy), runs the sm_100a kernel and writes the
+// destination window back.  Metering follows the reference call for call.
+namespace b200 {
+struct DeviceWindow {
+    wm_dmat d{};
+    explicit DeviceWindow(const MatView& v, bool upload, wm_ctx* ctx) {
+        check(wm_dev_alloc(ctx, v.rows * v.cols, &d.ptr));
+        d.rows = v.rows;
+        d.cols = v.cols;
+        d.ld = v.cols;
+        if (upload) check(wm_upload_u32(ctx, d, v.ptr, v.stride));
+    }
+    void download(const MatView& v, wm_ctx* ctx) const {
+        check(wm_download_u32(ctx, v.ptr, v.stride, d));
+    }
+    DeviceWindow(const DeviceWindow&) = delete;
+    DeviceWindow& operator=(const DeviceWindow&) = delete;
+    ~DeviceWindow() { wm_dev_free(d.ptr); }
+};
+inline bool trivial_scalar(Elem s, const Modulus& mod) {
+    return s == 0 || s == 1 || s == mod.minus_one();
+}
+}  // namespace b200
+
+inline void block_addsub(MatView dst, MatView a, MatView b, Elem sa, Elem sb, const Modulus& mod,
+                         CostMeter* meter = nullptr) {
+    if (a.rows != b.rows || a.cols != b.cols || dst.rows != a.rows || dst.cols != a.cols)
+        throw dimension_error("block_addsub dimension mismatch");
+    if (!dst.same_window(a) && dst.overlaps(a))
+        throw partial_overlap_error("block_addsub: dst partially overlaps a");
+    if (!dst.same_window(b) && dst.overlaps(b))
+        throw partial_overlap_error("block_addsub: dst partially overlaps b");
+    wm_ctx* ctx = b200::context(mod.p());
+    b200::DeviceWindow da(a, true, ctx);
+    std::optional<b200::DeviceWindow> db, dd;
+    if (!b.same_window(a)) db.emplace(b, true, ctx);
+    const wm_dmat& bd = db ? db->d : da.d;
+    const wm_dmat* dstd = dst.same_window(a) ? &da.d : dst.same_window(b) ? &bd : nullptr;
+    if (!dstd) {
+        dd.emplace(dst, false, ctx);
+        dstd = &dd->d;
+    }
+    b200::check(wm_block_addsub(ctx, *dstd, da.d, bd, sa, sb));
+    b200::check(wm_download_u32(ctx, dst.ptr, dst.stride, *dstd));
+    if (meter) {
+        meter->count_adds(dst.words());
+        if (!b200::trivial_scalar(sa, mod)) meter->count_mults(dst.words());
+        if (!b200::trivial_scalar(sb, mod)) meter->count_mults(dst.words());
+    }
+}
+
+inline void block_scale_copy(MatView dst, MatView src, Elem s, const Modulus& mod,
+                             CostMeter* meter = nullptr) {
+    if (dst.rows != src.rows || dst.cols != src.cols)
+        throw dimension_error("block_scale_copy dimension mismatch");
+    if (!dst.same_window(src) && dst.overlaps(src))
+        throw partial_overlap_error("block_scale_copy: dst partially overlaps src");
+    wm_ctx* ctx = b200::context(mod.p());
+    b200::DeviceWindow ds(src, true, ctx);
+    std::optional<b200::DeviceWindow> dd;
+    if (!dst.same_window(src)) dd.emplace(dst, false, ctx);
+    const wm_dmat& dstd = dd ? dd->d : ds.d;
+    b200::check(wm_block_scale_copy(ctx, dstd, ds.d, s));
+    b200::check(wm_download_u32(ctx, dst.ptr, dst.stride, dstd));
+    if (meter) {
+        if (s == 1 || s == mod.minus_one()) meter->count_moves(dst.words());
+        else meter->count_mults(dst.words());
+    }
+}
+
+inline void classical_mul(MatView C, MatView A, MatView B, Elem alpha, Elem beta,
+                          const Modulus& mod, CostMeter* meter = nullptr) {
+    const std::size_t m = A.rows, k = A.cols, n = B.cols;
+    if (B.rows != k || C.rows != m || C.cols != n)
+        throw dimension_error("classical_mul dimension mismatch");
+    if (C.overlaps(A) || C.overlaps(B))
+        throw alias_error("classical_mul: C must be disjoint from A and B");
+    wm_ctx* ctx = b200::context(mod.p());
+    b200::DeviceWindow da(A, true, ctx), dc(C, beta != 0, ctx);
+    std::optional<b200::DeviceWindow> db;
+    if (!B.same_window(A)) db.emplace(B, true, ctx);
+    b200::check(wm_classical_mul(ctx, dc.d, da.d, db ? db->d : da.d, alpha, beta));
+    dc.download(C, ctx);
+    if (meter) {
+        meter->on_classical();
+        meter->count_mults(static_cast<std::uint64_t>(m) * k * n);
+        meter->count_adds(static_cast<std::uint64_t>(m) * n * (k - 1));
+        if (beta != 0) meter->count_adds(static_cast<std::uint64_t>(m) * n);
+        if (!b200::trivial_scalar(alpha, mod)) meter->count_mults(static_cast<std::uint64_t>(m) * n);
+        if (!b200::trivial_scalar(beta, mod)) meter->count_mults(static_cast<std::uint64_t>(m) * n);
+    }
+}
+
 // ---- schedule DSL (schedule.hpp:261-684, executor.hpp:304-342) -------------
 // A parsed schedule is carried as its validated text; the device planner
 // re-reads it (it is small) at each run.
+// schedule.hpp:185-211
+enum class Contract : std::uint8_t { ReadOnly, OverwriteA, OverwriteB, OverwriteBoth };
+inline const char* contract_name(Contract c) {
+    switch (c) {
+        case Contract::ReadOnly: return "read-only";
+        case Contract::OverwriteA: return "overwrite-A";
+        case Contract::OverwriteB: return "overwrite-B";
+        case Contract::OverwriteBoth: return "overwrite-both";
+    }
+    return "?";
+}
+
 struct Schedule {
     std::string name;
     std::string text;       // canonical rendering (parses back to the same schedule)
     bool builtin_match = false;
+    // header fields of the rendering (schedule.hpp:219-224)
+    Contract contract = Contract::ReadOnly;
+    bool accumulating = false;
+    bool square_only = true;
 };
+
+namespace b200 {
+inline Schedule from_rendering(const std::string& text) {
+    Schedule s;
+    s.text = text;
+    std::istringstream is(text);
+    std::string line;
+    while (std::getline(is, line)) {
+        std::istringstream ls(line);
+        std::string key, val;
+        ls >> key >> val;
+        if (key == "schedule") s.name = val;
+        else if (key == "accumulating") s.accumulating = val == "true";
+        else if (key == "shape") s.square_only = val == "square";
+        else if (key == "contract")
+            for (Contract c : {Contract::ReadOnly, Contract::OverwriteA, Contract::OverwriteB,
+                               Contract::OverwriteBoth})
+                if (val == contract_name(c)) s.contract = c;
+    }
+    return s;
+}
+}  // namespace b200
 
 inline Schedule parse_schedule(const std::string& text) {
     int need = 0, match = 0;
@@ -349,11 +644,8 @@ inline Schedule parse_schedule(const std::string& text) {
     std::string out(static_cast<std::size_t>(need) + 1, '\0');
     b200::check(wm_parse_schedule(text.c_str(), &out[0], need + 1, &need, &match));
     out.resize(static_cast<std::size_t>(need));
-    Schedule s;
-    s.text = out;
+    Schedule s = b200::from_rendering(out);
     s.builtin_match = match != 0;
-    const auto sp = out.find(' '), nl = out.find('\n');
-    s.name = out.substr(sp + 1, nl - sp - 1);
     return s;
 }
 
@@ -365,7 +657,9 @@ inline Schedule builtin(const std::string& name) {
     std::string out(static_cast<std::size_t>(need) + 1, '\0');
     b200::check(wm_render_schedule(name.c_str(), &out[0], need + 1, &need));
     out.resize(static_cast<std::size_t>(need));
-    return {name, out, true};
+    Schedule s = b200::from_rendering(out);
+    s.builtin_match = true;
+    return s;
 }
 
 inline CostReport run_parsed_schedule(const Schedule& s, Matrix& A, Matrix& B, Matrix& C,
@@ -442,6 +736,25 @@ inline Matrix read_binary(std::istream& is) {
 }
 
 namespace models {
+// "blocked_acc_t<T>[_acc2]" (models.hpp:180-200)
+struct BlockedSpec {
+    int t = 1;
+    std::string base = "acc3";
+};
+inline std::optional<BlockedSpec> parse_blocked(const std::string& v) {
+    const std::string pre = "blocked_acc_t";
+    if (v.compare(0, pre.size(), pre) != 0) return std::nullopt;
+    std::size_t i = pre.size();
+    while (i < v.size() && v[i] >= '0' && v[i] <= '9') ++i;
+    if (i == pre.size()) return std::nullopt;
+    BlockedSpec b;
+    b.t = std::stoi(v.substr(pre.size(), i - pre.size()));
+    const std::string tail = v.substr(i);
+    if (tail == "_acc2") b.base = "acc2";
+    else if (!tail.empty()) return std::nullopt;
+    return b;
+}
+
 // expected_costs (models.hpp:202-229)
 inline CostReport expected_costs(const std::string& variant, std::size_t m, std::size_t k,
                                  std::size_t n, int cutoff) {

@@ -173,6 +173,22 @@ def ref_run_variant(variant, A, B, C0, alpha=1, beta=0, cutoff=1, p=DEFAULT_P):
     return A, B, Cm, report, calls
 
 
+def ref_primitive_on_windows(op, buf, wins, s0, s1=0, p=DEFAULT_P):
+    """One reference primitive (0 block_addsub, 1 block_scale_copy, 2 classical_mul)
+    on windows {r0, c0, rows, cols} of ONE buffer; returns (code, buffer after)."""
+    L = ref()
+    f = L.ref_primitive_on_windows
+    f.argtypes = [C.c_int, u64, u64, u32, P_u32, P_u64, u32, u32, C.c_char_p, C.c_int]
+    f.restype = C.c_int
+    out = np.array(buf, dtype=np.uint32, order="C")
+    w = np.zeros(12, dtype=np.uint64)
+    for i, win in enumerate(wins):
+        w[4 * i:4 * i + 4] = win
+    err = C.create_string_buffer(512)
+    rc = f(op, out.shape[0], out.shape[1], p, out.reshape(-1), w, s0, s1, err, 512)
+    return rc, out
+
+
 def ref_expected_costs(variant, m, k, n, cutoff):
     rep = np.zeros(6, dtype=np.uint64)
     err = C.create_string_buffer(512)

@@ -174,6 +174,31 @@ int ref_block_addsub(std::uint64_t r, std::uint64_t c, std::uint32_t p,
     }
 }
 
+// One primitive on windows of ONE buffer (rows x cols, row-major): the
+// aliasing / overlap rules of block_addsub, block_scale_copy and classical_mul
+// (ring.hpp:241-384) need views that share storage.  op 0 = block_addsub(dst, a,
+// b, s0, s1), 1 = block_scale_copy(dst, a, s0), 2 = classical_mul(dst, a, b, s0,
+// s1); win = {r0, c0, rows, cols} for dst, a, b.  The buffer is updated in place.
+int ref_primitive_on_windows(int op, std::uint64_t rows, std::uint64_t cols, std::uint32_t p,
+                             std::uint32_t* buf, const std::uint64_t* win, std::uint32_t s0,
+                             std::uint32_t s1, char* err, int errlen) {
+    try {
+        Modulus mod(p);
+        Matrix M(rows, cols, mod);
+        std::memcpy(M.data(), buf, rows * cols * sizeof(Elem));
+        auto w = [&](int i) { return M.view().window(win[4 * i], win[4 * i + 1], win[4 * i + 2],
+                                                     win[4 * i + 3]); };
+        if (op == 0) block_addsub(w(0), w(1), w(2), s0, s1, mod);
+        else if (op == 1) block_scale_copy(w(0), w(1), s0, mod);
+        else classical_mul(w(0), w(1), w(2), s0, s1, mod);
+        std::memcpy(buf, M.data(), rows * cols * sizeof(Elem));
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return code_of(e);
+    }
+}
+
 void ref_fill_random(std::uint32_t* out, std::uint64_t count, std::uint64_t seed,
                      std::uint32_t p) {
     SplitMix64 g(seed);

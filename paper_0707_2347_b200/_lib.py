@@ -26,7 +26,7 @@ EXPORTS = [
     "wm_run_parsed_schedule", "wm_parse_schedule", "wm_render_schedule",
     "wm_run_parsed_schedule_host_u32", "wm_matrix_file_info", "wm_matrix_read_host",
     "wm_matrix_write_host", "wm_matrix_read_device", "wm_matrix_write_device",
-    "wm_plan_report_parsed",
+    "wm_plan_report_parsed", "wm_lincomb", "wm_dev_alloc", "wm_dev_free",
 ]
 
 
@@ -68,6 +68,7 @@ def lib():
     L.wm_block_addsub.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, u32, u32]
     L.wm_block_scale_copy.argtypes = [ctx_p, wm_dmat, wm_dmat, u32]
     L.wm_classical_mul.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, u32, u32]
+    L.wm_lincomb.argtypes = [ctx_p, wm_dmat, i32, P(wm_dmat), P(u32)]
     L.wm_run_variant.argtypes = [ctx_p, C.c_char_p, wm_dmat, wm_dmat, wm_dmat, u32, u32, i32,
                                  P(wm_report)]
     L.wm_ipmm.argtypes = [ctx_p, wm_dmat, wm_dmat, wm_dmat, i32, P(wm_report)]

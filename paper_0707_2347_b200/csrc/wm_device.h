@@ -59,9 +59,22 @@ struct MulParams {
     unsigned long long* tl;  // measurement timeline slot (nullptr: off)
 };
 
+// dst <- sum_t coef[t] * src[t] (t < n <= kMaxLincomb), one pass (wm_lincomb)
+constexpr int kMaxLincomb = 4;
+struct LincombParams {
+    double* dst;
+    const double* src[kMaxLincomb];
+    std::uint64_t ldd, lds[kMaxLincomb];
+    double coef[kMaxLincomb];  // MODP: residues in [0, p); REAL64: values
+    std::uint64_t rows, cols;
+    int n;
+    double p;
+};
+
 // kernels (wm_kernels.cu, wm_dmma.cu, wm_i8.cu, wm_frame.cu)
 cudaError_t launch_addsub(const AddBatch& b, bool real, unsigned blocks, cudaStream_t s);
 cudaError_t launch_leaf_dmma(const MulParams& P, bool real, cudaStream_t s);
+cudaError_t launch_lincomb(const LincombParams& L, bool real, cudaStream_t s);
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,
                               std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
                               cudaStream_t s);

@@ -156,6 +156,43 @@ __global__ void k_fill_splitmix(double* __restrict__ dst, std::uint64_t ld, std:
     }
 }
 
+// dst = sum_i coef_i * src_i over up to kMaxLincomb equally shaped blocks in one
+// HBM pass (the S_i / T_i operand of a distributed product is a combination of
+// up to four quadrants; the gathered P_i folds into C with alpha * coef).
+// Canonical residues times coefficients < 2^16 sum to < 2^34: exact in float64.
+template <bool REAL, bool VEC>
+__global__ void __launch_bounds__(256) k_lincomb(const LincombParams L) {
+    const std::uint64_t cols = VEC ? L.cols / 2 : L.cols;
+    const std::uint64_t total = L.rows * cols;
+    const double p = L.p, pinv = 1.0 / L.p;
+    for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+         i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+        const std::uint64_t r = i / cols, c = (i - r * cols) * (VEC ? 2 : 1);
+        double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < kMaxLincomb; ++t) {
+            if (t >= L.n) break;
+            const double* src = L.src[t] + r * L.lds[t] + c;
+            if (VEC) {
+                const double2 x = __ldg(reinterpret_cast<const double2*>(src));
+                v0 = fma(L.coef[t], x.x, v0);
+                v1 = fma(L.coef[t], x.y, v1);
+            } else {
+                v0 = fma(L.coef[t], __ldg(src), v0);
+            }
+        }
+        if (!REAL) {  // v is an exact integer, |v| < 2^36
+            v0 = fma(-floor(v0 * pinv), p, v0);
+            v0 = v0 < 0.0 ? v0 + p : (v0 >= p ? v0 - p : v0);
+            v1 = fma(-floor(v1 * pinv), p, v1);
+            v1 = v1 < 0.0 ? v1 + p : (v1 >= p ? v1 - p : v1);
+        }
+        double* dst = L.dst + r * L.ldd + c;
+        if (VEC) *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        else *dst = v0;
+    }
+}
+
 unsigned grid_for(std::uint64_t total) {
     std::uint64_t b = (total + 255) / 256;
     if (b > 148ull * 32) b = 148ull * 32;
@@ -208,6 +245,21 @@ cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaSt
     cfg.numAttrs = 1;
     if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G, tl);
     return cudaLaunchKernelEx(&cfg, k_group<false>, gid, G, tl);
+}
+
+cudaError_t launch_lincomb(const LincombParams& L, bool real, cudaStream_t s) {
+    bool vec = L.cols % 2 == 0 && L.ldd % 2 == 0 && reinterpret_cast<std::uintptr_t>(L.dst) % 16 == 0;
+    for (int t = 0; t < L.n; ++t)
+        vec = vec && L.lds[t] % 2 == 0 && reinterpret_cast<std::uintptr_t>(L.src[t]) % 16 == 0;
+    const unsigned grid = grid_for(L.rows * (vec ? L.cols / 2 : L.cols));
+    if (vec) {
+        if (real) k_lincomb<true, true><<<grid, 256, 0, s>>>(L);
+        else k_lincomb<false, true><<<grid, 256, 0, s>>>(L);
+    } else {
+        if (real) k_lincomb<true, false><<<grid, 256, 0, s>>>(L);
+        else k_lincomb<false, false><<<grid, 256, 0, s>>>(L);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,

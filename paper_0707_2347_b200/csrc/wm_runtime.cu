@@ -1483,7 +1483,12 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         }
     if (!cp) {
         PlanOptions opt;
-        opt.fuse_frames = ctx->fuse_frames && frame_kernel_available();
+        // the fused frame kernels move 16-byte vectors and TMA boxes over the
+        // caller's blocks: they need even leading dimensions and 16-B aligned
+        // bases (every quadrant offset is then a multiple of 64 elements)
+        const bool frame_aligned = A.ld % 2 == 0 && B.ld % 2 == 0 && C.ld % 2 == 0 &&
+                                   aligned16(A.ptr) && aligned16(B.ptr) && aligned16(C.ptr);
+        opt.fuse_frames = ctx->fuse_frames && frame_kernel_available() && frame_aligned;
         opt.parsed = parsed;
         auto np = std::make_unique<CachedPlan>();
         np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld, alpha,
@@ -1491,7 +1496,24 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         if (np->plan.arena_words)
             WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
         double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
-        np->steps = lower(np->plan, base, *ctx);
+        try {
+            np->steps = lower(np->plan, base, *ctx);
+        } catch (const Error& e) {
+            // a frame GEMM the tensor-map path cannot describe: plan again with
+            // every frame unfused (nothing has been issued yet)
+            if (e.code != E_INVALID || !opt.fuse_frames) throw;
+            opt.fuse_frames = false;
+            const std::uint64_t had = np->plan.arena_words;
+            np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld,
+                                    alpha, beta, cutoff, opt);
+            if (np->plan.arena_words > had) {
+                WM_CUDA(cudaFree(np->arena));
+                np->arena = nullptr;
+                WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
+                base[3] = np->arena;
+            }
+            np->steps = lower(np->plan, base, *ctx);
+        }
         if (io) {
             const wm_dmat M[3] = {A, B, C};
             add_io_steps(np->steps, *io, M, ctx->f.p);
@@ -1841,7 +1863,7 @@ int wm_block_scale_copy(wm_ctx* ctx, wm_dmat dst, wm_dmat src, uint32_t s) {
             fail(E_DIMENSION, "block_scale_copy dimension mismatch");
         if (!d.same_window(v) && d.overlaps(v))
             fail(E_PARTIAL_OVERLAP, "block_scale_copy: dst partially overlaps src");
-        if (s % ctx->f.p == 1 && d.same_window(v)) return;
+        if (ctx->f.is_one(modp_scalar(ctx->f, s)) && d.same_window(v)) return;
         Op op{};
         op.kind = OP_COPY;
         op.d = d;
@@ -1854,6 +1876,34 @@ int wm_block_scale_copy(wm_ctx* ctx, wm_dmat dst, wm_dmat src, uint32_t s) {
         st.add.it[0] = t;
         st.add.n = 1;
         WM_CUDA(launch_addsub(st.add, ctx->f.real, item_blocks(t), ctx->stream));
+    });
+}
+
+int wm_lincomb(wm_ctx* ctx, wm_dmat dst, int n, const wm_dmat* src, const uint32_t* coef) {
+    return guard([&] {
+        if (n < 1 || n > kMaxLincomb || !src || !coef) fail(E_INVALID, "lincomb takes 1..4 terms");
+        check_dmat(dst, "dst");
+        const View d = raw_view(dst);
+        LincombParams L{};
+        L.dst = dst.ptr;
+        L.ldd = dst.ld;
+        L.rows = dst.rows;
+        L.cols = dst.cols;
+        L.n = n;
+        L.p = static_cast<double>(ctx->f.p);
+        for (int t = 0; t < n; ++t) {
+            check_dmat(src[t], "src");
+            if (src[t].rows != dst.rows || src[t].cols != dst.cols)
+                fail(E_DIMENSION, "lincomb dimension mismatch");
+            const View v = raw_view(src[t]);
+            if (!d.same_window(v) && d.overlaps(v))
+                fail(E_PARTIAL_OVERLAP, "lincomb: dst partially overlaps a source");
+            L.src[t] = src[t].ptr;
+            L.lds[t] = src[t].ld;
+            const Scalar sc = modp_scalar(ctx->f, coef[t]);
+            L.coef[t] = ctx->f.real ? sc.d : static_cast<double>(sc.r);
+        }
+        WM_CUDA(launch_lincomb(L, ctx->f.real, ctx->stream));
     });
 }
 
@@ -2204,6 +2254,18 @@ int wm_plan_schedule_calls(char* out, int len) {
         out[len - 1] = 0;
     }
     return static_cast<int>(g_sched_calls.size());
+}
+
+int wm_dev_alloc(wm_ctx* ctx, uint64_t words, double** out) {
+    return guard([&] {
+        if (!out || !words) fail(E_INVALID, "wm_dev_alloc: empty request");
+        WM_CUDA(cudaSetDevice(ctx->device));
+        WM_CUDA(cudaMalloc(out, words * sizeof(double)));
+    });
+}
+
+void wm_dev_free(double* p) {
+    if (p) cudaFree(p);
 }
 
 int wm_upload_u32(wm_ctx* ctx, wm_dmat dst, const uint32_t* host, uint64_t host_ld) {

@@ -1,4 +1,4 @@
-"""Multi-GPU product partition of the top one or two Winograd levels.
+"""Multi-GPU product partition of the top Winograd levels.
 
 One process per GPU.  The root rank holds A, B, C.  The top level uses the
 Table-1 (std2) formulas:
@@ -9,23 +9,36 @@ Table-1 (std2) formulas:
     T1 = B12-B11  T2 = B22-T1  T3 = B22-B12  T4 = T2-B21
     C11 = P1+P2   C12 = P1+P6+P5+P3   C21 = P1+P6+P7-P4   C22 = P1+P6+P7+P5
 
-With two levels the same formulas are applied again to each S_i / T_i, giving
-49 products P_(i,j) of quarter size; P_(i,j) folds into sub-quadrant q2 of C
-quadrant q1 with coefficient C_COEF[i][q1] * C_COEF[j][q2].  Product t is owned
-by rank t mod G.  The root forms each remote product's
-operands (S_i, T_i) and sends them (point-to-point, NCCL over NVLink on GPUs);
-every rank computes its products with the single-GPU memory-lean plan of the
-local schedule (C-ABI run_variant); the P_i come back to the root, which folds
-each one into the C quadrants as it arrives (alpha, beta applied once).  The
-network carries only operand blocks and products, as north_star specifies.
+With L levels the formulas are applied again to each operand, giving 7^L
+products P_(i1..iL) of size n/2^L; P_(i1..iL) folds into the nested
+sub-quadrant (q1..qL) of C with coefficient prod_l C_COEF[i_l][q_l].
+Product t (in `product_indices` order) is owned by rank t mod G.
 
-The exchange logic is backend-agnostic: ``CudaBackend`` runs the block
-combinations and products through libwinomem_b200 on the rank's GPU; tests
-drive the same protocol on CPU tensors over gloo with an injected product.
+Protocol (NCCL over NVLink on GPUs; gloo in the CPU tests):
+  1. the root broadcasts A and B (one collective each);
+  2. every rank forms its own operands S_t, T_t from its copy with the one-pass
+     combination kernel (wm_lincomb: up to four quadrants per level), so no rank
+     waits for the root to build operands;
+  3. every rank multiplies them with the single-GPU memory-lean plan (the
+     in-place schedule `ip` on square operands: the operands are scratch
+     copies, so the local product needs no temporaries at all);
+  4. remote products go back to the root with non-blocking sends in product
+     order; the root scales C by beta once and folds alpha * coef * P_t straight
+     into the C blocks as each product arrives -- no full-size accumulator.
+     The root keeps at most `window` receives posted, in product order, which is
+     also each sender's order, so every pair of ranks sees its messages in the
+     same order on its channel (no cross-ordering deadlock).
+The network carries only the operand sources and the products, as north_star
+specifies.  Every rank reports the peak extra bytes it held (operand copies,
+operands, products, receive buffers, plus the local plan's temporaries).
+
+The exchange logic is backend-agnostic: ``CudaBackend`` runs the combinations,
+folds and products through libwinomem_b200 on the rank's GPU; tests drive the
+same protocol on CPU tensors over gloo with an injected product.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Callable, List, Sequence, Tuple
 
 import torch
@@ -40,6 +53,8 @@ T_COEF = [(1, 0, 0, 0), (0, 0, 1, 0), (0, 0, 0, 1), (1, -1, -1, 1), (-1, 1, 0, 0
 C_COEF = [(1, 1, 1, 1), (1, 0, 0, 0), (0, 1, 0, 0), (0, 0, -1, 0), (0, 1, 0, 1), (0, 1, 1, 1),
           (0, 0, 1, 1)]
 
+MAX_LEVELS = 3
+
 
 def owner(i: int, world: int) -> int:
     return i % world
@@ -50,6 +65,10 @@ def quads(M: torch.Tensor) -> List[torch.Tensor]:
     return [M[:r, :c], M[:r, c:], M[r:, :c], M[r:, c:]]
 
 
+def _bytes(t: torch.Tensor) -> int:
+    return t.numel() * t.element_size()
+
+
 @dataclass
 class TorchModP:
     """Reference backend on torch tensors (any device): exact residue arithmetic
@@ -57,26 +76,26 @@ class TorchModP:
     p: int
     mm: Callable[[torch.Tensor, torch.Tensor], torch.Tensor]
 
-    def lincomb(self, coefs: Sequence[int], blocks: Sequence[torch.Tensor]) -> torch.Tensor:
-        out = torch.zeros_like(blocks[0])
-        for c, b in zip(coefs, blocks):
-            if c:
-                out = out + c * b
+    def lincomb(self, terms: Sequence[Tuple[int, torch.Tensor]]) -> torch.Tensor:
+        out = torch.zeros_like(terms[0][1])
+        for c, b in terms:
+            out = out + c * b
         return torch.remainder(out, self.p)
 
-    def product(self, X: torch.Tensor, Y: torch.Tensor) -> torch.Tensor:
-        return self.mm(X, Y)
+    def product(self, X: torch.Tensor, Y: torch.Tensor) -> Tuple[torch.Tensor, int]:
+        return self.mm(X, Y), 0
+
+    def scale(self, Cq: torch.Tensor, beta: int):
+        Cq.copy_(torch.remainder(beta * Cq, self.p))
 
     def fold(self, Cq: torch.Tensor, coef: int, P: torch.Tensor):
         Cq.copy_(torch.remainder(Cq + coef * P, self.p))
 
-    def finish(self, Cq: torch.Tensor, acc: torch.Tensor, alpha: int, beta: int):
-        Cq.copy_(torch.remainder(alpha * acc + beta * Cq, self.p))
-
 
 class CudaBackend:
-    """libwinomem_b200 on this rank's GPU: block combinations with the block
-    addition kernels, products with the single-GPU memory-lean plan."""
+    """libwinomem_b200 on this rank's GPU: operand combinations and folds with
+    the one-pass combination kernel, products with the single-GPU memory-lean
+    plan of `variant`."""
 
     def __init__(self, p: int, variant: str, cutoff: int, device: int, real: bool = False):
         from . import winomem as W
@@ -88,38 +107,24 @@ class CudaBackend:
     def _mat(self, t: torch.Tensor):
         return self.W.Matrix.wrap(t, self.W.Modulus(self.p), real=self.real)
 
-    def lincomb(self, coefs, blocks):
-        W = self.W
-        out = torch.empty_like(blocks[0])
-        terms = [(c % self.m, b) for c, b in zip(coefs, blocks) if c]
-        O = self._mat(out)
-        first = True
-        for c, b in terms:
-            Bm = self._mat(b)
-            if first:
-                W.block_scale_copy(O.view(), Bm.view(), c)
-                first = False
-            else:
-                W.block_addsub(O.view(), O.view(), Bm.view(), 1, c)
+    def lincomb(self, terms):
+        out = torch.empty_like(terms[0][1])
+        self.W.lincomb(self._mat(out).view(), [(c % self.m, self._mat(b).view()) for c, b in terms])
         return out
 
     def product(self, X, Y):
         out = torch.empty((X.shape[0], Y.shape[1]), dtype=X.dtype, device=X.device)
-        self.W.run_variant(self.variant, self._mat(X), self._mat(Y), self._mat(out),
-                           alpha=1, beta=0, cutoff=self.cutoff)
-        return out
+        rep = self.W.run_variant(self.variant, self._mat(X), self._mat(Y), self._mat(out),
+                                 alpha=1, beta=0, cutoff=self.cutoff)
+        return out, rep.peak_extra_bytes
 
-    def zero(self, Cq):
-        Cq.zero_()
+    def scale(self, Cq, beta):
+        M = self._mat(Cq)
+        self.W.block_scale_copy(M.view(), M.view(), beta % self.m)
 
     def fold(self, Cq, coef, P):
         M = self._mat(Cq)
         self.W.block_addsub(M.view(), M.view(), self._mat(P).view(), 1, coef % self.m)
-
-    def finish(self, Cq, acc, alpha, beta):
-        M = self._mat(Cq)
-        self.W.block_addsub(M.view(), self._mat(acc).view(), M.view(), alpha % self.m,
-                            beta % self.m)
 
 
 def product_indices(levels: int) -> List[Tuple[int, ...]]:
@@ -131,116 +136,153 @@ def product_indices(levels: int) -> List[Tuple[int, ...]]:
     return out
 
 
-def _operand(M, idx, coef, backend):
-    """S_idx(A) / T_idx(B) through the levels: quadrant combination of the
-    previous level's operand."""
+def operand(M, idx, table, backend, stats=None):
+    """S_idx(A) / T_idx(B): one combination of at most four quadrants per level
+    (each level's block is freed once the next one is formed; the result stays
+    held in `stats`)."""
     X = M
     for i in idx:
-        X = backend.lincomb(coef[i], quads(X))
+        Y = backend.lincomb([(c, q) for c, q in zip(table[i], quads(X)) if c])
+        if stats is not None:
+            stats.hold(_bytes(Y))
+            if X is not M:
+                stats.release(_bytes(X))
+        X = Y
     return X
 
 
-def _target(acc_quads, idx):
-    """(accumulator block, coefficient) a product P_idx folds into: P_(i1,i2)
-    adds C_COEF[i1][q1] * C_COEF[i2][q2] * P to sub-quadrant q2 of quadrant q1."""
-    out = []
-    for q1 in range(4):
-        c1 = C_COEF[idx[0]][q1]
-        if not c1:
-            continue
-        if len(idx) == 1:
-            out.append((acc_quads[q1], c1))
-            continue
-        for q2 in range(4):
-            c2 = C_COEF[idx[1]][q2]
-            if c2:
-                out.append((quads(acc_quads[q1])[q2], c1 * c2))
+def targets(C, idx):
+    """(block of C, coefficient) pairs product P_idx folds into."""
+    out = [(C, 1)]
+    for i in idx:
+        out = [(quads(blk)[q], coef * C_COEF[i][q]) for blk, coef in out for q in range(4)
+               if C_COEF[i][q]]
     return out
 
 
+@dataclass
+class PartitionStats:
+    """What one rank did: the products it computed, the peak extra device bytes
+    it held at once (beyond the root's caller-owned A, B, C), and its traffic."""
+    products: List[int] = field(default_factory=list)
+    peak_extra_bytes: int = 0
+    bytes_sent: int = 0
+    bytes_received: int = 0
+    _live: int = 0
+
+    def hold(self, nbytes: int, transient: int = 0):
+        self._live += nbytes
+        self.peak_extra_bytes = max(self.peak_extra_bytes, self._live + transient)
+
+    def release(self, nbytes: int):
+        self._live -= nbytes
+
+
 def partitioned_multiply(A, B, C, alpha: int, beta: int, backend, group=None, root: int = 0,
-                         levels: int = 1):
+                         levels: int = 1, window: int = 2) -> PartitionStats:
     """C <- alpha*A*B + beta*C with the 7^levels products of the top `levels`
-    Winograd levels (7 or 49) spread over the ranks of `group` (product t on
-    rank t mod G).  A, B, C are only read on the root; other ranks pass None
-    (their shapes are broadcast).  Returns the products computed locally, keyed
-    by their index in product_indices(levels)."""
-    if levels not in (1, 2):
-        raise ValueError("levels must be 1 (7 products) or 2 (49 products)")
+    Winograd levels spread over the ranks of `group` (product t on rank t mod
+    G).  A, B, C are only read on the root; other ranks pass None (shapes are
+    broadcast)."""
+    if levels < 1 or levels > MAX_LEVELS:
+        raise ValueError(f"levels must be 1..{MAX_LEVELS}")
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
-    meta = torch.zeros(4, dtype=torch.int64)
-    dev = A.device if rank == root else None
+    gr = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    stats = PartitionStats()
+    meta = torch.zeros(3, dtype=torch.int64)
     if rank == root:
-        meta[:] = torch.tensor([A.shape[0], A.shape[1], B.shape[1], 0])
-    if dist.get_backend(group) == "nccl":
+        meta[:] = torch.tensor([A.shape[0], A.shape[1], B.shape[1]])
+    nccl = dist.get_backend(group) == "nccl"
+    if nccl:
         meta = meta.cuda()
-    dist.broadcast(meta, src=root, group=group)
-    m, k, n = (int(x) for x in meta[:3].tolist())
-    if rank != root:
-        dev = meta.device if meta.is_cuda else torch.device("cpu")
+    dist.broadcast(meta, src=gr(root), group=group)
+    m, k, n = (int(x) for x in meta.tolist())
     f = 2 ** levels
-    b_m, b_k, b_n = m // f, k // f, n // f
+    if m % f or k % f or n % f:
+        raise ValueError(f"{m}x{k}x{n} does not split into {f}x{f} blocks")
+    dev = A.device if rank == root else (meta.device if nccl else torch.device("cpu"))
+
+    # 1. operand sources to every rank
+    if rank != root:
+        A = torch.empty((m, k), dtype=torch.float64, device=dev)
+        B = torch.empty((k, n), dtype=torch.float64, device=dev)
+        stats.hold(_bytes(A) + _bytes(B))
+        stats.bytes_received += _bytes(A) + _bytes(B)
+    dist.broadcast(A, src=gr(root), group=group)
+    dist.broadcast(B, src=gr(root), group=group)
+
     prods = product_indices(levels)
     mine = [t for t in range(len(prods)) if owner(t, world) == rank]
+    stats.products = mine
+    remote = [t for t in range(len(prods)) if owner(t, world) != rank] if rank == root else []
+    pshape = (m // f, n // f)
+    pbytes = (m // f) * (n // f) * 8
 
+    # 2. the root: C <- beta*C once, then receives posted in product order
+    posted: List[Tuple[int, torch.Tensor, object]] = []
+    nxt = 0
     if rank == root:
-        acc = [torch.zeros((m // 2, n // 2), dtype=A.dtype, device=dev) for _ in range(4)]
-        # operands of remote products go out first so remote ranks start early
-        reqs, keep = [], []
-        for t, idx in enumerate(prods):
-            o = owner(t, world)
-            if o == root:
-                continue
-            X = _operand(A, idx, S_COEF, backend)
-            Y = _operand(B, idx, T_COEF, backend)
-            keep += [X, Y]
-            reqs.append(dist.isend(X, dst=o, group=group))
-            reqs.append(dist.isend(Y, dst=o, group=group))
-        # post every product receive now: a remote rank may finish its first
-        # product before the root has handed out all operands
-        pending = []
-        for t, idx in enumerate(prods):
-            o = owner(t, world)
-            if o == root:
-                continue
-            P = torch.empty((b_m, b_n), dtype=A.dtype, device=dev)
-            pending.append((idx, P, dist.irecv(P, src=o, group=group)))
-        local = {}
-        for t in mine:
-            idx = prods[t]
-            P = backend.product(_operand(A, idx, S_COEF, backend), _operand(B, idx, T_COEF, backend))
-            local[t] = P
-            for blk, coef in _target(acc, idx):
-                backend.fold(blk, coef, P)
-        for idx, P, req in pending:
-            req.wait()
-            for blk, coef in _target(acc, idx):
-                backend.fold(blk, coef, P)
-        for r in reqs:
-            r.wait()
-        Cq = quads(C)
-        for q in range(4):
-            backend.finish(Cq[q], acc[q], alpha, beta)
-        return local
-    local = {}
+        for blk in quads(C):
+            backend.scale(blk, beta)
+
+        def post():
+            nonlocal nxt
+            t = remote[nxt]
+            buf = torch.empty(pshape, dtype=torch.float64, device=dev)
+            stats.hold(pbytes)
+            posted.append((t, buf, dist.irecv(buf, src=gr(owner(t, world)), group=group)))
+            nxt += 1
+
+        while nxt < len(remote) and len(posted) < window:
+            post()
+
+    def fold(t, P):
+        for blk, coef in targets(C, prods[t]):
+            backend.fold(blk, alpha * coef, P)
+
+    # 3. local products
+    sends = []
     for t in mine:
-        X = torch.empty((b_m, b_k), dtype=torch.float64, device=dev)
-        Y = torch.empty((b_k, b_n), dtype=torch.float64, device=dev)
-        dist.recv(X, src=root, group=group)
-        dist.recv(Y, src=root, group=group)
-        P = backend.product(X, Y)
-        local[t] = P
-        dist.send(P, dst=root, group=group)
-    return local
+        X = operand(A, prods[t], S_COEF, backend, stats)
+        Y = operand(B, prods[t], T_COEF, backend, stats)
+        P, plan_peak = backend.product(X, Y)
+        stats.hold(_bytes(P), transient=plan_peak)
+        stats.release(_bytes(X) + _bytes(Y))
+        del X, Y
+        if rank == root:
+            fold(t, P)
+            stats.release(_bytes(P))
+        else:
+            sends.append((P, dist.isend(P, dst=gr(root), group=group)))
+            stats.bytes_sent += _bytes(P)
+
+    # 4. the root folds the remote products as they arrive
+    while posted:
+        t, buf, req = posted.pop(0)
+        req.wait()
+        stats.bytes_received += pbytes
+        fold(t, buf)
+        stats.release(pbytes)
+        del buf
+        if nxt < len(remote):
+            post()
+    for P, req in sends:
+        req.wait()
+    if rank != root:
+        del A, B
+    return stats
 
 
 def local_variant(variant: str, m: int, k: int, n: int) -> str:
-    """Schedule for the plain products P_i = S_i T_i on each rank."""
-    if variant == "ipmm":
-        return "ipmm"
-    if variant in ("ip", "ovl", "ovl2", "ovr", "iprect", "ipovmm", "aclr"):
-        return "ip" if m == k == n else "iprect"
+    """Schedule for the plain products P_t = S_t T_t on each rank.  S_t and T_t
+    are freshly formed scratch copies, so the in-place schedule may overwrite
+    them: `ip` on squares (zero temporaries, whatever the caller's variant),
+    `iprect` for the rectangle it supports, std2 otherwise."""
+    if m == k == n:
+        return "ip"
+    if k <= min(m, n) and m % k == 0 and n % k == 0:
+        return "iprect"
     return "std2"
 
 
@@ -250,8 +292,10 @@ def makespan_bound(world: int, products: int = 7) -> float:
     return products / per
 
 
-def choose_levels(world: int) -> int:
-    """7 products when they already fill the ranks as well as 49 would (G = 1,
-    7, 8: same makespan, fewer and larger products); 49 otherwise (G = 2: 1.96x
-    instead of 1.75x, G = 4: 3.77x instead of 3.5x)."""
-    return 1 if makespan_bound(world, 7) >= makespan_bound(world, 49) else 2
+def choose_levels(world: int, n: int = 1 << 30, cutoff: int = 1) -> int:
+    """The fewest levels (7, 49 or 343 products) whose makespan bound is within
+    2% of the best one, while each product stays above the cutoff: G = 2 -> 49
+    (1.96x), G = 4 -> 343 (3.99x), G = 7 -> 7, G = 8 -> 343 (7.98x vs 7.0x)."""
+    usable = [L for L in range(1, MAX_LEVELS + 1) if (n >> L) >= max(2 * cutoff, 2)] or [1]
+    best = max(makespan_bound(world, 7 ** L) for L in usable)
+    return next(L for L in usable if makespan_bound(world, 7 ** L) >= 0.98 * best)

@@ -391,6 +391,17 @@ def block_scale_copy(dst: MatView, src: MatView, s, mod: Modulus = None):
     ctx.leave()
 
 
+def lincomb(dst: MatView, terms, mod: Modulus = None):
+    """dst <- sum coef * src over 1..4 (coef, MatView) terms in one pass
+    (wm_lincomb); dst may alias a source exactly."""
+    ctx = _ctx_of(dst.mat)
+    n = len(terms)
+    srcs = (_lib.wm_dmat * n)(*[v.dmat() for _, v in terms])
+    coefs = (C.c_uint32 * n)(*[int(c) & 0xFFFFFFFF for c, _ in terms])
+    _check(_lib.lib().wm_lincomb(ctx.h, dst.dmat(), n, srcs, coefs))
+    ctx.leave()
+
+
 def classical_mul(Cv: MatView, Av: MatView, Bv: MatView, alpha, beta, mod: Modulus = None):
     ctx = _ctx_of(Cv.mat)
     _check(_lib.lib().wm_classical_mul(ctx.h, Cv.dmat(), Av.dmat(), Bv.dmat(), alpha, beta))

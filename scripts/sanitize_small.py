@@ -12,8 +12,10 @@ from oracle import oracle as O  # noqa: E402
 
 ctx = W.Context.get()
 ctx.set_option("graphs", 0)  # plain launches: the sanitizer sees every kernel
+ctx.set_option("dag", 3)     # the three concurrent issue lanes of the product path
 bad = 0
-for (v, n, c, acc) in [("std2", 512, 128, False), ("acc2", 512, 128, True), ("ip", 512, 128, False),
+for (v, n, c, acc) in [("std2", 1024, 128, False),  # config 1: 49 fused frames
+                       ("std2", 512, 128, False), ("acc2", 512, 128, True), ("ip", 512, 128, False),
                        ("aclr", 512, 128, True), ("ipmm", 512, 128, False), ("acc3", 512, 128, True)]:
     for leaf in (2, 0):
         ctx.set_option("leaf_kernel", leaf)

@@ -93,6 +93,51 @@ def test_golden_small_cases(W, golden, options):
     assert seen > (300 if not options else 100)
 
 
+def test_error_goldens_through_capi(W, O):
+    """The reference's illegal calls (tests/golden/error_cases.json, generated
+    from oracle/_ref) through the C-ABI on the device: run_variant on device
+    matrices and on host u32 buffers raise the reference's exception class; the
+    primitives on windows of ONE device matrix reject partial overlap / aliasing
+    exactly where the reference does and otherwise leave the same buffer."""
+    g = json.load(open(os.path.join(GOLD, "error_cases.json")))
+    E = W.winomem
+    for c in g["variant_cases"]:
+        v, m, k, n = c["variant"], c["m"], c["k"], c["n"]
+        acc = c["beta"] != 0 or _acc(v)
+        a, b = O.fill_random(m, k, c["seed"]), O.fill_random(k, n, c["seed"] + 1)
+        c0 = O.fill_random(m, n, c["seed"] + 2) if acc else np.zeros((m, n), np.uint32)
+        A, B, C = W.Matrix(m, k), W.Matrix(k, n), W.Matrix(m, n)
+        A.from_u32(a)
+        B.from_u32(b)
+        C.from_u32(c0)
+        args = dict(alpha=c["alpha"], beta=c["beta"], cutoff=c["cutoff"])
+        if c["error"]:
+            with pytest.raises(E.WinomemError) as ei:
+                W.run_variant(v, A, B, C, **args)
+            assert ei.value.code == c["error"], c
+            ch = c0.copy()
+            with pytest.raises(E.WinomemError) as ei:
+                W.run_variant_host(v, a.copy(), b.copy(), ch, c["alpha"], c["beta"], c["cutoff"])
+            assert ei.value.code == c["error"], c
+        else:
+            W.run_variant(v, A, B, C, **args)
+            assert "%016x" % C.hash() == c["c_hash"], c
+    ops = {0: lambda w, s0, s1: W.block_addsub(w[0], w[1], w[2], s0, s1),
+           1: lambda w, s0, s1: W.block_scale_copy(w[0], w[1], s0),
+           2: lambda w, s0, s1: W.classical_mul(w[0], w[1], w[2], s0, s1)}
+    for c in g["primitive_cases"]:
+        M = W.Matrix(c["rows"], c["cols"])
+        M.from_u32(O.fill_random(c["rows"], c["cols"], c["seed"]))
+        wins = [M.view().window(*w) for w in c["windows"]]
+        if c["error"]:
+            with pytest.raises(E.WinomemError) as ei:
+                ops[c["op"]](wins, c["s0"], c["s1"])
+            assert ei.value.code == c["error"], c
+        else:
+            ops[c["op"]](wins, c["s0"], c["s1"])
+            assert "%016x" % M.hash() == c["buf_hash"], c
+
+
 def test_primitive_kats(W):
     E = W.winomem
     a = W.Matrix(2, 2, W.Modulus(65521)).from_u32(np.array([[1, 2], [3, 4]], dtype=np.uint32))
@@ -162,9 +207,15 @@ def test_config_full_size_hash(W, name, fused):
     c = CFG[name]
     want = c["appendix_a"]
     A, B, C = _problem(W, c["m"], c["k"], c["n"], c["seed"], bool(c["beta"]))
+    a_before, b_before = A.hash(), B.hash()
     rep = W.run_variant(c["variant"], A, B, C, alpha=c["alpha"], beta=c["beta"],
                         cutoff=c["cutoff"])
     assert "%016x" % C.hash() == want
+    # the read-only contracts at full size (executor.hpp:40-49, acceptance.cpp:238-244):
+    # C1 std2, C2 acc2 and C4 ipmm must leave A and B bit-identical -- the fused
+    # frames park their planes in dead blocks, never in A or B
+    if c["variant"] in ("std2", "acc2", "ipmm"):
+        assert A.hash() == a_before and B.hash() == b_before, name
     e = W.expected_costs(c["variant"], c["m"], c["k"], c["n"], c["cutoff"])
     assert rep.peak_extra_words == e.peak_extra_words
     assert rep.peak_extra_bytes == 8 * e.peak_extra_words
@@ -223,9 +274,48 @@ def test_real64_winograd_frobenius(W, O):
         assert err <= 1e-12 * 2 ** depth, (n, cutoff, err)
 
 
+def test_real64_config5_full_size(W, O):
+    """Config 5 at full size: float64 std2, 32768^3, cutoff 1024 (depth 5), inputs
+    uniform[-1,1) from seeds 5 / 6.  ||C - AB||_F / ||AB||_F estimated with 8
+    Gaussian probes (E ||dC x||^2 = ||dC||_F^2; AB x applied as A (B x)), stated
+    tolerance 1e-12 * 2^5; then an exact-shape comparison at 8192 (cutoff 256,
+    depth 5) against the oracle's classical float64 product."""
+    import torch
+    n, cutoff, depth = 32768, 1024, 5
+    A = W.Matrix(n, n, real=True)
+    B = W.Matrix(n, n, real=True)
+    C = W.Matrix(n, n, real=True)
+    A.fill_random(5)
+    B.fill_random(6)
+    rep = W.run_variant("std2", A, B, C, cutoff=cutoff)
+    assert rep.peak_extra_words == W.expected_costs("std2", n, n, n, cutoff).peak_extra_words
+    g = torch.Generator(device=C.t.device).manual_seed(99)
+    num = den = 0.0
+    for _ in range(8):
+        x = torch.randn(n, 1, dtype=torch.float64, device=C.t.device, generator=g)
+        ref = A.t @ (B.t @ x)
+        num += float(((C.t @ x) - ref).square().sum())
+        den += float(ref.square().sum())
+    err = (num / den) ** 0.5
+    assert err <= 1e-12 * 2 ** depth, err
+    del A, B, C
+    torch.cuda.empty_cache()
+    n, cutoff = 8192, 256
+    A = W.Matrix(n, n, real=True)
+    B = W.Matrix(n, n, real=True)
+    C = W.Matrix(n, n, real=True)
+    A.fill_random(5)
+    B.fill_random(6)
+    W.run_variant("std2", A, B, C, cutoff=cutoff)
+    a, b = O.real_fill(n, n, 5), O.real_fill(n, n, 6)
+    ref = O.classical_f64(a, b)
+    err = np.linalg.norm(C.t.cpu().numpy() - ref) / np.linalg.norm(ref)
+    assert err <= 1e-12 * 2 ** depth, err
+
+
 @pytest.mark.parametrize("shape", [(128, 32, 64), (128, 128, 128), (256, 256, 256),
                                    (384, 96, 192), (512, 1024, 128), (1024, 1024, 1024),
-                                   (128, 16384, 64)])
+                                   (128, 16384, 64), (128, 32768, 64)])
 @pytest.mark.parametrize("engine", [0, 1], ids=["cpasync", "tma"])
 def test_leaf_i8_vs_oracle(W, O, shape, engine):
     """tcgen05 int8-limb leaf kernel on tile-aligned shapes (incl. the long-K limb bound),
@@ -239,7 +329,9 @@ def test_leaf_i8_vs_oracle(W, O, shape, engine):
         m, k, n = shape
         for (al, be) in [(1, 0), (1, 1), (3, 65520), (65520, 7)]:
             A, B, C = _problem(W, m, k, n, m + k + n + al, True)
-            if k == 16384:  # worst case for the limb accumulators: all residues p-1
+            if k >= 16384:  # worst case for the limb accumulators: all residues p-1
+                # (k = 32768: the cross accumulator A_h B_l + A_l B_h exceeds 2^31
+                # and is read back as u32 -- the wrap the kernel relies on)
                 A.t.fill_(65520.0)
                 B.t.fill_(65520.0)
             a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
@@ -395,3 +487,28 @@ def test_run_parsed_hand_written_schedule(W, O):
         plan = W.winomem.plan_report_parsed(mod.SWAPPED, m, k, n, c, 5, 0)
         assert (rep.mults, rep.adds, rep.peak_extra_words) == (plan.mults, plan.adds,
                                                               plan.peak_extra_words)
+
+
+def test_reference_acceptance_gate_on_b200():
+    """The reference's own acceptance gate (proj/tests/acceptance/acceptance.cpp),
+    compiled against the drop-in include/winomem_b200.hpp with only its include
+    lines changed (tests/cpp/make_acceptance.py; criteria 5-6 -- validator and
+    pebble search, out of scope -- stubbed), runs on the B200: criteria 1
+    (oracle correctness, 20 seeds, within 60 s), 2 (exact op counts), 3 (peaks and
+    allocation totals), 4 (contracts) and 7 (n = 2048 op-count gating) pass."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.join(root, "tests", "cpp"))
+    import make_acceptance
+    exe = make_acceptance.build()
+    if exe is None:
+        pytest.skip("acceptance binary not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    out = r.stdout
+    os.makedirs(os.path.join(root, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(root, "gpurun_out", "acceptance_b200.log"), "w") as f:
+        f.write(out + r.stderr)
+    for crit in ("1", "2", "3", "4", "7"):
+        line = next((l for l in out.splitlines() if f"criterion {crit} " in l), None)
+        assert line is not None and line.startswith("[PASS]"), (crit, out)

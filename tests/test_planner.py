@@ -89,6 +89,20 @@ def test_expected_costs_match_reference_directly(W, O):
         same("ipovmm", m, k, n, 8)
 
 
+def test_error_goldens_through_planner(W):
+    """The reference's illegal run_variant calls (tests/golden/error_cases.json,
+    from oracle/_ref) raise the same exception class in the host planner."""
+    g = json.load(open(os.path.join(GOLD, "error_cases.json")))
+    for c in g["variant_cases"]:
+        args = (c["variant"], c["m"], c["k"], c["n"], c["cutoff"], c["alpha"], c["beta"])
+        if c["error"]:
+            with pytest.raises(W.winomem.WinomemError) as ei:
+                W.plan_report(*args)
+            assert ei.value.code == c["error"], c
+        else:
+            W.plan_report(*args)
+
+
 # SURVEY.md Appendix A / B and 8(d): config-level plans
 CONFIGS = [
     # variant, m, k, n, cutoff, beta, peak words, frames, leaves
