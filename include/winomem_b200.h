@@ -113,8 +113,7 @@ int wm_ctx_sync(wm_ctx* ctx);
  *   "dag" [3]           issue lanes (concurrent streams); "epoch" [512] launches per join
  *   "stream_io" [1]     host u32 boundary streamed through the graph (pinned buffers)
  *   "leaf_kernel" [2]   0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto
- *   "direct_frames" [1], "gemm_engine" [0], "multicast" [0], "frame_cfg" [0]   GEMM engines
- *   "coop_frames" [0], "post_fold" [0]   measured-slower alternatives
+ *   "direct_frames" [1], "gemm_engine" [0]   GEMM engines (direct-limb frames; TMA / cp.async leaves)
  *   "pdl" [1], "prep_rows" [1], "comb_block" [128]   launch attributes / shapes
  *   "trace" [0]         per-launch timeline (wm_diag_trace)
  *   "subset" [0]        measurement only: 0 all launches, 1 additions only,

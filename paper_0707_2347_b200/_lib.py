@@ -10,7 +10,11 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libwinomem_b200.so")
+PRODUCT_LIB = os.path.join(HERE, "libwinomem_b200.so")
+# the same library plus the measurement-only wm_diag_* probes (build.py); the
+# measurement scripts select it with WM_DIAG=1, the product never does
+DIAG_LIB = os.path.join(HERE, "libwinomem_b200_diag.so")
+LIB_PATH = DIAG_LIB if os.environ.get("WM_DIAG") == "1" else PRODUCT_LIB
 
 # status codes (winomem_b200.h)
 WM_OK = 0
@@ -100,6 +104,24 @@ def lib():
                                                   P(wm_report)]
     _lib = L
     return L
+
+
+_diag = None
+
+
+def diag_lib():
+    """The diagnostics library on its own (own contexts): kernel-level checks
+    that need a wm_diag_* entry point without switching the product library."""
+    global _diag
+    if _diag is None:
+        if not os.path.exists(DIAG_LIB):
+            raise ImportError(f"{DIAG_LIB} is missing (python -m paper_0707_2347_b200.build)")
+        L = C.CDLL(DIAG_LIB)
+        L.wm_ctx_create.argtypes = [C.c_int, C.c_uint32, C.c_int, C.c_void_p, C.POINTER(C.c_void_p)]
+        L.wm_ctx_destroy.argtypes = [C.c_void_p]
+        L.wm_last_error.restype = C.c_char_p
+        _diag = L
+    return _diag
 
 
 def last_error():

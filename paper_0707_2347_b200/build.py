@@ -1,4 +1,6 @@
-"""Build the native library ``libwinomem_b200.so`` in-tree for sm_100a.
+"""Build the native library ``libwinomem_b200.so`` in-tree for sm_100a (and
+``libwinomem_b200_diag.so``: the same library plus the measurement-only probes
+and wm_diag_* exports that scripts/ and one kernel-level test use).
 
     python -m paper_0707_2347_b200.build        (or __graft_entry__.build())
 
@@ -29,22 +31,29 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", CSRC, "
 COMMON += os.environ.get("WM_NVCC_FLAGS", "").split()
 
 
+# measurement-only probes: linked into libwinomem_b200_diag.so, never the product
+DIAG_ONLY = {"wm_diag.cu"}
+DIAG_LIB = os.path.join(HERE, "libwinomem_b200_diag.so")
+
+
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
 def _headers():
     return (glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
-            glob.glob(os.path.join(INC, "*.h")))
+            glob.glob(os.path.join(CSRC, "*.inc")) + glob.glob(os.path.join(INC, "*.h")))
 
 
-def _compile(src, hdr_mtime, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(job, hdr_mtime, verbose):
+    src, diag = job
+    obj = os.path.join(OBJ, os.path.basename(src) + (".diag.o" if diag else ".o"))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj
-    cmd = [NVCC] + ARCH + COMMON + ["-c", src, "-o", obj]
+    flags = COMMON + (["-DWM_DIAG=1"] if diag else [])
+    cmd = [NVCC] + ARCH + flags + ["-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, "-x", "cu"] + ARCH + COMMON + ["-c", src, "-o", obj]
+        cmd = [NVCC, "-x", "cu"] + ARCH + flags + ["-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,16 +70,21 @@ def build(verbose=False, jobs=None):
     gen_fusion.main()
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     srcs = _sources()
+    runtime = os.path.join(CSRC, "wm_runtime.cu")
+    jobs_ = [(s_, False) for s_ in srcs] + [(runtime, True)]
     with cf.ThreadPoolExecutor(max_workers=jobs or min(8, os.cpu_count() or 1)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, hdr_mtime, verbose), srcs))
-    if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
-        return LIB
-    cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs
-    if verbose:
-        print(" ".join(cmd), flush=True)
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode != 0:
-        raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+        objs = dict(zip(jobs_, ex.map(lambda j: _compile(j, hdr_mtime, verbose), jobs_)))
+    product = [objs[(s_, False)] for s_ in srcs if os.path.basename(s_) not in DIAG_ONLY]
+    diag = [objs[(s_, False)] for s_ in srcs if s_ != runtime] + [objs[(runtime, True)]]
+    for lib, parts in ((LIB, product), (DIAG_LIB, diag)):
+        if os.path.exists(lib) and os.path.getmtime(lib) >= max(os.path.getmtime(o) for o in parts):
+            continue
+        cmd = [NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + parts
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     return LIB
 
 

@@ -101,27 +101,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// multicast variant: the box lands at the same offset in every CTA of `mask`
-__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int x, int y,
-                                               int z, std::uint64_t* mbar, std::uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;\n" ::"r"(tc::smem_u32(dst)),
-        "l"(reinterpret_cast<std::uint64_t>(map)), "r"(x), "r"(y), "r"(z),
-        "r"(tc::smem_u32(mbar)), "h"(mask)
-        : "memory");
-}
-
-__device__ __forceinline__ std::uint32_t cluster_rank() {
-    std::uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
 // byte offset of B element (k, n) in a BN-byte-swizzled MN-major limb tile
 template <int BN>
 __device__ __forceinline__ std::uint32_t boff(std::uint32_t k, std::uint32_t n) {
@@ -204,10 +183,6 @@ __device__ __forceinline__ void direct_tile(const GemmParams& P, const TmaMaps& 
     const bool bconv = P.b[prod].fmt == 0;  // float64 B: split by the epilogue warps
     const bool blsu = !bconv && BSRC == 1;
     const GemmSrc Cd = P.c[prod];
-    const std::uint32_t mcn = P.mc_n, mcm = P.mc_m;
-    const bool mc = mcn * mcm > 1;
-    const std::uint32_t crank = mc ? cluster_rank() : 0;
-    const std::uint32_t cy = crank % mcn, cz = crank / mcn;
     if (warp == 0) {
         if (lane == 0) {
             const bool btma = !bconv && !blsu;
@@ -218,25 +193,10 @@ __device__ __forceinline__ void direct_tile(const GemmParams& P, const TmaMaps& 
                     tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
                 tc::mbar_arrive_expect_tx(&S.full[st], bytes);
                 const int k0 = static_cast<int>(kc * KT);
-                if (!mc) {
-                    tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
-                    if (btma)
-                        tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0,
-                                    0, &S.full[st]);
-                } else {
-                    const std::uint32_t ra = BM / mcn, rb = KT / mcm;
-                    const std::uint16_t amask = static_cast<std::uint16_t>(((1u << mcn) - 1) << (cz * mcn));
-                    std::uint16_t bmask = 0;
-                    for (std::uint32_t z = 0; z < mcm; ++z) bmask |= static_cast<std::uint16_t>(1u << (cy + z * mcn));
-                    for (int limb = 0; limb < 2; ++limb) {
-                        tma_load_3d_mc(S.stage[st] + limb * A_PART + cy * ra * KT, &M.a[prod], k0,
-                                       static_cast<int>(i0 + cy * ra), limb, &S.full[st], amask);
-                        if (btma)
-                            tma_load_3d_mc(S.stage[st] + 2 * A_PART + limb * C::B_PART + cz * rb * BN,
-                                           &M.b[prod], static_cast<int>(j0),
-                                           static_cast<int>(k0 + cz * rb), limb, &S.full[st], bmask);
-                    }
-                }
+                tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
+                if (btma)
+                    tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0, 0,
+                                &S.full[st]);
             }
         }
     } else if (warp == 1) {
@@ -359,12 +319,6 @@ __global__ void __launch_bounds__(NT, 1)
     const std::uint32_t j0 = blockIdx.y * BN;
     const bool bconv = P.b[prod].fmt == 0;  // float64 B: split by the epilogue warps
     const bool blsu = !bconv && BSRC == 1;
-    // TMA multicast: a cluster spans mc_n N tiles x mc_m M tiles of one product;
-    // each CTA fetches 1/mc_n of the A rows (shared along N) and 1/mc_m of the
-    // B K-rows (shared along M) and multicasts them, so one SM's TMA unit walks
-    // 192 instead of 512 box rows per stage.  Only used when no stage is reused
-    // (nk <= NS), so no cross-CTA "empty" handshake is needed.
-    const bool mc = P.mc_n * P.mc_m > 1;
 
     if (tid == 32) WM_DSTAMP(0);
     if (warp == 0) tc::tmem_alloc(&S.tmem_base, C::TCOLS);
@@ -379,7 +333,6 @@ __global__ void __launch_bounds__(NT, 1)
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if (mc) cluster_sync_all();  // peers' barriers are initialised before any multicast lands
     const std::uint32_t tbase = S.tmem_base;
     if (tid == 32) WM_DSTAMP(1);
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
@@ -392,123 +345,8 @@ __global__ void __launch_bounds__(NT, 1)
     tc::fence_before();
     __syncthreads();
     WM_TL_END(P.tl);
-    if (mc) cluster_sync_all();  // no CTA leaves while a peer's multicast may still target it
     if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
     if (tid == 32) WM_DSTAMP(7);
-}
-
-// ---- one fused leaf frame in ONE launch ------------------------------------
-//
-// The three launches of a fused frame (prep, seven-product GEMM, combine) as
-// phases of one grid of one CTA per SM, separated by two grid-wide barriers:
-// the launch gaps between them (~1 us each on the measured critical path) and
-// the GEMM's setup (TMEM allocation, barrier init -- done before the prep phase
-// here) leave the chain.  Co-residency: one CTA per SM (the GEMM ring fills the
-// shared memory), launched cooperatively; the runtime never runs two of these
-// at once (they share a pseudo resource in the dependency analysis).
-
-// Sense-reversing grid barrier on a per-launch {count, sense} pair; the sense
-// returns to its initial value after the kernel's two barriers, so the pair is
-// reusable by every replay of the launch.
-__device__ __forceinline__ std::uint32_t ld_acquire(const std::uint32_t* p) {
-    std::uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Arrival is a fire-and-forget release reduction on a monotonic counter; the
-// last arriver of generation g sees (g+1) * grid and flips the sense word the
-// others poll.  The counter is rewound by the last CTA of the launch's second
-// barrier (`rewind`), so every replay starts from zero.
-__device__ __forceinline__ void grid_barrier(std::uint32_t* bar, std::uint32_t target, bool rewind) {
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic writes -> later TMA reads
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const std::uint32_t s = ld_acquire(bar + 1);
-        std::uint32_t old;
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(bar) : "memory");
-        if (old == target - 1) {
-            if (rewind) atomicExch(bar, 0u);
-            asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(s ^ 1u) : "memory");
-        } else {
-            unsigned long long t0, t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-            while (ld_acquire(bar + 1) == s) {
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-                if (t - t0 > 2000000000ull) __trap();  // a lost peer: fail loudly, never hang
-            }
-        }
-    }
-    __syncthreads();
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
-template <int BN>
-__global__ void __launch_bounds__(NT, 1)
-    k_frame_coop(const __grid_constant__ FramePrepParams PP, const __grid_constant__ GemmParams GP,
-                 const __grid_constant__ FrameCombParams CP, const __grid_constant__ TmaMaps M,
-                 std::uint32_t* bar) {
-    using C = DCfg<BN>;
-    constexpr int NS = C::NS;
-    extern __shared__ std::uint8_t smem_raw[];
-    const std::uint32_t base = tc::smem_u32(smem_raw);
-    DSmem<BN>& S = *reinterpret_cast<DSmem<BN>*>(smem_raw + ((1024 - (base & 1023)) & 1023));
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const std::uint32_t nt = GP.n / BN;
-    const std::uint32_t ntiles = nt * GP.tiles_m * GP.nprod;
-    const bool has_tile = blockIdx.x < ntiles;
-    const std::uint32_t z = blockIdx.x / nt;
-    const int prod = has_tile ? static_cast<int>(z / GP.tiles_m) : 0;
-    const std::uint32_t i0 = (z % GP.tiles_m) * BM, j0 = (blockIdx.x % nt) * BN;
-    const bool bconv = GP.b[prod].fmt == 0;
-    if (has_tile) {
-        if (warp == 0) tc::tmem_alloc(&S.tmem_base, C::TCOLS);
-        if (tid == 32) {
-            for (int s = 0; s < NS; ++s) {
-                tc::mbar_init(&S.full[s], bconv ? 1 + NEPI / 32 : 1);
-                tc::mbar_init(&S.empty[s], 1);
-            }
-            tc::mbar_init(&S.done, 1);
-            tc::mbar_fence_init();
-        }
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    const std::uint32_t tbase = S.tmem_base;
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    WM_TL_BEGIN(PP.tl);
-
-    // phase 1: prep, whole rows per CTA (every row's reads precede its writes)
-    const std::uint32_t c = PP.c, half = c / 2;
-    const std::uint32_t rows = NT / half;
-    for (std::uint32_t r0 = blockIdx.x * rows; r0 < c; r0 += gridDim.x * rows) {
-        const std::uint32_t r = r0 + tid / half;
-        const bool act = static_cast<std::uint32_t>(tid) < rows * half && r < c;
-        const std::uint64_t j = 2 * (tid % half);
-        fdev::PrepRegs R;
-        if (act) fdev::prep_limbs_load(PP, r, j, R);
-        __syncthreads();
-        if (act) fdev::prep_limbs_store(PP, r, j, R);
-    }
-    grid_barrier(bar, gridDim.x, false);
-
-    // phase 2: one product tile per CTA
-    if (has_tile) direct_tile<BN, 0>(GP, M, S, tbase, prod, i0, j0, false);
-    tc::fence_before();
-    grid_barrier(bar, 2 * gridDim.x, true);
-    tc::fence_after();
-    if (has_tile && warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
-
-    // phase 3: U-chain combine over column pairs
-    const std::uint64_t total = static_cast<std::uint64_t>(c) * half;
-    for (std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(NT) + tid; idx < total;
-         idx += static_cast<std::uint64_t>(gridDim.x) * NT) {
-        const std::uint64_t r = idx / half, j = 2 * (idx - r * half);
-        fdev::comb_pair<true>(CP, r, j);
-    }
-    WM_TL_END(PP.tl);
-    WM_PDL_LATE_C();
 }
 
 template <int BN>
@@ -530,51 +368,20 @@ cudaError_t dlaunch(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = dsmem_bytes<BN>();
     cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
-    int na = 1;
-    if (P.mc_n * P.mc_m > 1) {
-        attr[1].id = cudaLaunchAttributeClusterDimension;
-        attr[1].val.clusterDim.x = 1;
-        attr[1].val.clusterDim.y = P.mc_n;
-        attr[1].val.clusterDim.z = P.mc_m;
-        na = 2;
-    }
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, k_gemm_direct<BN, BSRC>, P, M);
-}
-
-int g_sms = 0;
-bool g_coop_ok = false;
-
-template <int BN>
-cudaError_t coop_launch(const FramePrepParams& PP, const GemmParams& GP, const FrameCombParams& CP,
-                        const TmaMaps& M, std::uint32_t* bar, cudaStream_t s) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(g_sms));
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = dsmem_bytes<BN>();
-    cfg.stream = s;
-    // not a cooperative launch (measured: +2 us of launch gap): co-residency of
-    // the one-CTA-per-SM grid only needs the SMs' current tenants to finish,
-    // and nothing that could wait on this grid is resident before it completes
-    // (its programmatic dependents launch after every CTA's final trigger)
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_frame_coop<BN>, PP, GP, CP, M, bar);
+    return cudaLaunchKernelEx(&cfg, k_gemm_direct<BN, BSRC>, P, M);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_denc = nullptr;
 
 // 3-D byte map over a limb-plane pair: {cols, rows, 2 limbs}; box_l limbs per box
 bool encode_planes(CUtensorMap* map, const GemmSrc& src, std::uint64_t cols, std::uint64_t rows,
-                   std::uint32_t box_c, std::uint32_t box_r, CUtensorMapSwizzle sw,
-                   std::uint32_t box_l = 2) {
+                   std::uint32_t box_c, std::uint32_t box_r, CUtensorMapSwizzle sw) {
+    const std::uint32_t box_l = 2;
     cuuint64_t dims[3] = {cols, rows, 2};
     cuuint64_t strides[2] = {src.ld, src.part};
     cuuint32_t box[3] = {box_c, box_r, box_l};
@@ -604,17 +411,6 @@ cudaError_t gemm_direct_init() {
     if ((e = dset_attr<32, 1>()) != cudaSuccess) return e;
     if ((e = dset_attr<64, 1>()) != cudaSuccess) return e;
     g_direct_ok = true;
-    // single-launch frames: one CTA per SM must fit next to nothing else
-    int dev = 0, sms = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-        cudaFuncSetAttribute(k_frame_coop<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(dsmem_bytes<32>())) == cudaSuccess &&
-        cudaFuncSetAttribute(k_frame_coop<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(dsmem_bytes<64>())) == cudaSuccess) {
-        g_sms = sms;
-        g_coop_ok = true;
-    }
     return cudaSuccess;
 }
 
@@ -638,14 +434,12 @@ bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M) {
     const CUtensorMapSwizzle bsw = bn == 32   ? CU_TENSOR_MAP_SWIZZLE_32B
                                    : bn == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
                                               : CU_TENSOR_MAP_SWIZZLE_128B;
-    const bool mc = P.mc_n * P.mc_m > 1;
-    const std::uint32_t mn = mc ? P.mc_n : 1, mm = mc ? P.mc_m : 1, bl = mc ? 1 : 2;
     for (std::uint32_t i = 0; i < P.nprod; ++i) {
-        if (!encode_planes(&M.a[i], P.a[i], P.k, P.m, KT, BM / mn,
-                           KT == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B, bl))
+        if (!encode_planes(&M.a[i], P.a[i], P.k, P.m, KT, BM,
+                           KT == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B))
             return false;
         if (P.b[i].fmt == 2 &&
-            !encode_planes(&M.b[i], P.b[i], P.n, P.k, static_cast<std::uint32_t>(bn), KT / mm, bsw, bl))
+            !encode_planes(&M.b[i], P.b[i], P.n, P.k, static_cast<std::uint32_t>(bn), KT, bsw))
             return false;
     }
     return true;
@@ -665,18 +459,6 @@ int gemm_direct_choose(const GemmParams& P) {
     return P.n % widest == 0 ? widest : P.n % 64 == 0 ? 64 : 32;
 }
 
-// Multicast cluster for a direct launch (sets P.mc_n / P.mc_m): up to 4 N tiles
-// x 2 M tiles of one product, only when every K stage has its own ring slot.
-void gemm_direct_cluster(GemmParams& P, int bn, bool enable) {
-    bn %= 1000;
-    P.mc_n = P.mc_m = 1;
-    const int ns = bn == 128 ? DCfg<128>::NS : DCfg<32>::NS;
-    if (!enable || bn == 128 || P.k / KT > static_cast<std::uint32_t>(ns)) return;
-    const std::uint32_t nt = P.n / bn;
-    P.mc_n = nt % 4 == 0 ? 4 : nt % 2 == 0 ? 2 : 1;
-    P.mc_m = P.tiles_m % 2 == 0 ? 2 : 1;
-}
-
 // bn: 32 / 64; + 1000 selects cp.async B loads instead of TMA
 cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s) {
     switch (bn) {
@@ -685,29 +467,6 @@ cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cu
         case 128: return dlaunch<128, 0>(P, M, s);
         case 1032: return dlaunch<32, 1>(P, M, s);
         case 1064: return dlaunch<64, 1>(P, M, s);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-// Single-launch fused frame (k_frame_coop): the direct GEMM's product set and
-// tiling must fit one wave of one CTA per SM, with plane operands only (no
-// float64 B) and a row of the prep within one CTA.
-bool frame_coop_supported(const GemmParams& P, int bn) {
-    if (!g_coop_ok || (bn != 32 && bn != 64) || !gemm_direct_supported(P, bn)) return false;
-    if (P.m != P.n || P.m != P.k || P.m / 2 > static_cast<std::uint32_t>(NT) ||
-        P.mc_n * P.mc_m > 1)
-        return false;
-    for (std::uint32_t i = 0; i < P.nprod; ++i)
-        if (P.b[i].fmt != 2) return false;
-    return (P.n / bn) * P.tiles_m * P.nprod <= static_cast<std::uint32_t>(g_sms);
-}
-
-cudaError_t launch_frame_coop(const FramePrepParams& PP, const GemmParams& GP,
-                              const FrameCombParams& CP, const TmaMaps& M, int bn,
-                              std::uint32_t* bar, cudaStream_t s) {
-    switch (bn) {
-        case 32: return coop_launch<32>(PP, GP, CP, M, bar, s);
-        case 64: return coop_launch<64>(PP, GP, CP, M, bar, s);
         default: return cudaErrorInvalidValue;
     }
 }

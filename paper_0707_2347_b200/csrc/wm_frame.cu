@@ -138,10 +138,7 @@ __global__ void __launch_bounds__(1024) k_frame_prep_limbs(const FramePrepParams
     WM_PDL_LATE_M();
 }
 
-// thread (r, 2 consecutive columns j, j+1) of the quadrant; POST: with a folded
-// run of the parent's additions (a separate instantiation keeps the plain
-// combine's registers and code small)
-template <bool POST>
+// thread (r, 2 consecutive columns j, j+1) of the quadrant
 __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
@@ -150,7 +147,7 @@ __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     if (idx < static_cast<std::uint64_t>(P.c) * c2) {
         const std::uint64_t r = idx / c2, j = 2 * (idx - r * c2);
-        fdev::comb_pair<false, POST>(P, r, j);
+        fdev::comb_pair<false>(P, r, j);
     }
     WM_TL_END(P.tl);
     WM_PDL_LATE_M();
@@ -185,9 +182,7 @@ cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
 }
 
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s) {
-    if (P.post.kind)
-        return launch_pdl(k_frame_comb<true>, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
-    return launch_pdl(k_frame_comb<false>, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
+    return launch_pdl(k_frame_comb, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
                       g_comb_block);
 }
 

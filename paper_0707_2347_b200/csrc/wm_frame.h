@@ -43,22 +43,6 @@ struct FramePrepParams {
     unsigned long long* tl;          // measurement timeline slot (nullptr: off)
 };
 
-// The parent schedule's run of additions right after the frame, folded into
-// its combine (lowering pass, wm_runtime.cu): every view has the frame's
-// output shape, so the combine thread that writes C positions (r, j), (r, j+c),
-// (r+c, j), (r+c, j+c) runs the run's dataflow on exactly those positions.
-struct FramePost {
-    int kind;                  // 0 none, 1 fused group `gid` (gen_fusion.py), 2 one addition
-    int gid;
-    fused::GroupParams g;
-    double* d;                 // kind 2: d = sa*a + sb*b (mode, wm_device.h)
-    const double* a;
-    const double* b;
-    std::uint64_t ldd, lda, ldb;
-    std::uint32_t mode;
-    double sa, sb;
-};
-
 struct FrameCombParams {
     const std::uint16_t* P[7];  // product planes (mod p)
     std::uint64_t pld[7];       // plane leading dimensions (uint16 elements)
@@ -67,21 +51,11 @@ struct FrameCombParams {
     std::uint32_t alpha, beta;  // beta != 0: packed beta*C_in in the C11 slots
     double pd, pinv;
     unsigned long long* tl;     // measurement timeline slot (nullptr: off)
-    FramePost post;
     std::uint32_t cin_f64;      // beta != 0: C_in read as float64 from C (no packing)
 };
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s);
 
-// One fused frame in a single cooperative launch (wm_direct.cu): prep, the
-// seven-product direct GEMM and the combine as phases between grid barriers;
-// `bar` is the launch's zero-initialised {count, sense} pair.
-struct GemmParams;
-struct TmaMaps;
-bool frame_coop_supported(const GemmParams& G, int bn);
-cudaError_t launch_frame_coop(const FramePrepParams& PP, const GemmParams& GP,
-                              const FrameCombParams& CP, const TmaMaps& M, int bn,
-                              std::uint32_t* bar, cudaStream_t s);
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s);
 
 }  // namespace wm

@@ -1,7 +1,6 @@
-// Device code of the fused leaf frames shared by the three-launch path
-// (wm_frame.cu) and the single-launch cooperative frame kernel (wm_direct.cu):
-// operand loading (incl. folded parent additions), the limb-plane prep of one
-// row and the U-chain combine of one column pair.
+// Device code of the fused leaf frames (wm_frame.cu): operand loading (incl.
+// folded parent additions), the limb-plane prep of one row and the U-chain
+// combine of one column pair.
 #pragma once
 
 #include <cstdint>
@@ -154,7 +153,7 @@ __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::
 // U2 = P1+P6, U3 = U2+P7, U4 = U2+P5, U5 = U4+P3, U6 = U3-P4, U7 = U3+P5 and
 // C_ij = alpha*U + beta*C_in.  CG: read the product planes and the packed C_in
 // through L2 (written by other CTAs of the same grid).
-template <bool CG, bool POST = true>
+template <bool CG>
 __device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_t r, std::uint64_t j) {
     const double p = P.pd, pinv = P.pinv;
     double pv[7][2];
@@ -207,31 +206,6 @@ __device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_
 #pragma unroll
     for (int qd = 0; qd < 4; ++qd)
         *reinterpret_cast<double2*>(P.C.q[qd] + r * P.C.ld + j) = make_double2(out[qd][0], out[qd][1]);
-    // the folded run of the parent schedule on the same four positions (its
-    // slots are this thread's own positions: plain loads see the stores above)
-    const FramePost& Q = P.post;
-    if (!POST || Q.kind == 0) return;
-    std::uint64_t rows[4], cols[4];
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-        rows[qd] = r + (qd >> 1) * static_cast<std::uint64_t>(P.c);
-        cols[qd] = j + (qd & 1) * static_cast<std::uint64_t>(P.c);
-    }
-    if (Q.kind == 1) {
-        fused::group_dispatch4<false>(Q.gid, Q.g, rows, cols);  // all loads before any store
-        return;
-    }
-    double2 a[4], b[4];
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd) {
-        a[qd] = *reinterpret_cast<const double2*>(Q.a + rows[qd] * Q.lda + cols[qd]);
-        b[qd] = *reinterpret_cast<const double2*>(Q.b + rows[qd] * Q.ldb + cols[qd]);
-    }
-#pragma unroll
-    for (int qd = 0; qd < 4; ++qd)
-        *reinterpret_cast<double2*>(Q.d + rows[qd] * Q.ldd + cols[qd]) =
-            make_double2(apply<false>(a[qd].x, b[qd].x, Q.mode, Q.sa, Q.sb, p, pinv),
-                         apply<false>(a[qd].y, b[qd].y, Q.mode, Q.sa, Q.sb, p, pinv));
 }
 
 }  // namespace fdev

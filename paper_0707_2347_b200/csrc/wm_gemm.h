@@ -27,7 +27,6 @@ struct GemmParams {
     std::uint32_t alpha, beta;  // float64 outputs only
     double pd, pinv;
     unsigned long long* trace;  // diagnostics: per-CTA phase timestamps (nullptr: off)
-    std::uint32_t mc_n, mc_m;   // direct engine: TMA-multicast cluster extent along N / M tiles
     unsigned long long* tl;     // measurement timeline slot (nullptr: off)
 };
 
@@ -51,7 +50,6 @@ cudaError_t gemm_direct_init();
 bool gemm_direct_supported(const GemmParams& P, int bn);
 bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M);
 int gemm_direct_choose(const GemmParams& P);
-void gemm_direct_cluster(GemmParams& P, int bn, bool enable);
 cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s);
 
 }  // namespace wm

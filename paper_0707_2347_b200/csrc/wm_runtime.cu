@@ -60,7 +60,7 @@ int set_err(int code, const std::string& msg) {
     } while (0)
 
 struct Step {
-    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB, FCOOP, UPLOAD, DOWNLOAD } kind;
+    enum Kind : std::uint8_t { ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB, UPLOAD, DOWNLOAD } kind;
     AddBatch add;
     unsigned blocks = 0;
     MulParams mul;
@@ -74,7 +74,6 @@ struct Step {
     int bn = 32, split = 1;
     std::shared_ptr<TmaMaps> tmaps;
     unsigned long long* tl = nullptr;  // GROUP: measurement timeline slot
-    std::uint32_t* bar = nullptr;      // FCOOP: the launch's grid-barrier pair
     // UPLOAD / DOWNLOAD (host u32 boundary): one block of a host matrix, staged
     // as u32 on the device and converted to / from the float64 operand
     std::uint32_t* hptr = nullptr;
@@ -108,8 +107,6 @@ void op_sets(const Op& o, std::vector<View>& rd, std::vector<View>& wr) {
 //   GEMM:    reads the planes in C (accumulating: also h1 / h2 and the float64
 //            B22 fallback in B);  writes the product planes in h0, h1
 //   combine: reads h0, h1 and the packed beta*C_in in C;  writes C
-constexpr std::uint8_t kGridRegion = 200;  // pseudo region: "all SMs" (cooperative frames)
-
 void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size_t first,
                 const View* ext = nullptr) {
     const bool acc = !f.is_zero(o.sb);
@@ -118,7 +115,7 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
     };
     for (std::size_t j = first; j < steps.size(); ++j) {
         Step& s = steps[j];
-        if (ext && s.kind != Step::FCOOP) {  // planes outside C: the prep never touches C
+        if (ext) {  // planes outside C: the prep never touches C
             if (s.kind == Step::FPREP) {
                 add(s.rd, o.a), add(s.rd, o.b);
                 for (int e = 0; e < 4; ++e) add(s.wr, ext[e]);
@@ -143,19 +140,6 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
             case Step::FCOMB:
                 add(s.rd, o.h0), add(s.rd, o.h1), add(s.rd, o.d), add(s.wr, o.d);
                 break;
-            case Step::FCOOP: {
-                op_sets(o, s.rd, s.wr);
-                if (ext)
-                    for (int e = 0; e < 4; ++e) add(s.wr, ext[e]);
-                // one cooperative frame at a time: its grid needs every SM
-                View grid;
-                grid.region = kGridRegion;
-                grid.origin = 0;
-                grid.rows = grid.cols = grid.ld = 1;
-                s.rd.push_back(grid);
-                s.wr.push_back(grid);
-                break;
-            }
             default: op_sets(o, s.rd, s.wr);
         }
     }
@@ -180,10 +164,8 @@ struct CachedPlan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     unsigned long long* tl = nullptr;  // measurement timeline (trace option)
-    std::uint32_t* bars = nullptr;     // grid-barrier pairs of the cooperative frames
     ~CachedPlan() {
         if (tl) cudaFree(tl);
-        if (bars) cudaFree(bars);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (arena) cudaFree(arena);
@@ -219,25 +201,19 @@ struct wm_ctx {
     int leaf_kernel = 2;  // 0 dmma, 1 i8, 2 auto (i8 where the tiles fit, else dmma)
     int subset = 0;       // measurement: 0 all, 1 adds, 2 leaves, 3 frames, 4/5/6 frame prep/gemm/comb
     int gemm_engine = 0;  // int8 GEMM operand path: 0 cp.async ring, 1 TMA tensor maps
-    int frame_cfg = 0;    // measurement: force the frame GEMM tiling (100*BN + split)
     bool fuse_adds = true;  // fused schedule runs (gen_fusion.py)
     bool direct_ok = false;  // direct-limb frame GEMM available (wm_direct.cu)
     bool direct_frames = true;  // use it for fused frames (limb-pair operand planes)
     int dag = 3;                // concurrent issue over this many streams (0/1: one stream;
                                 // measured: 3 >= 2, 4 > 8 lanes)
     bool fold = true;           // fold a frame's operand-producing additions into its prep
-    bool coop_frames = false;   // fused frames as one cooperative launch (k_frame_coop)
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
     bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
     bool cin_direct = true;     // accumulating frames: all planes in dead blocks, C_in read by the combine
-    bool post_fold = false;     // fold the parent's next additions into a frame's combine
-                                // (measured slower: C2 4.94 vs 4.69 ms, C4 85.5 vs 73.8 ms)
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
     const void* traced = nullptr;  // CachedPlan of the last traced run
-    bool multicast = false;     // direct frame GEMM: TMA multicast clusters (measured slower: the
-                                // SM ingress, not L2 or the issuing TMA unit, bounds the load)
     Lanes lanes;
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
@@ -427,8 +403,8 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, int force, bool direct, bool multicast, bool wide_plain,
-                 const View* ext = nullptr) {
+                 int engine, bool direct, bool wide_plain, const View* ext = nullptr) {
+    const int force = 0;
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
     const auto aq = quad_split(op.a), bq = quad_split(op.b), cq = quad_split(op.d);
@@ -555,7 +531,6 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
         if (force == 0 && wide_plain && (!acc || ext) && g.bn == 32 && G.n % 64 == 0 && G.m >= 256)
             g.bn = 64;
         auto maps = std::make_shared<TmaMaps>();
-        gemm_direct_cluster(G, g.bn, multicast);
         if (!gemm_direct_supported(G, g.bn) || !gemm_direct_encode(G, g.bn, *maps))
             fail(E_INVALID, "direct-limb frame GEMM: unsupported operands");
         g.tmaps = maps;
@@ -861,71 +836,6 @@ std::vector<View> choose_product_hosts(const Plan& plan, std::size_t i, const Fo
     return out;
 }
 
-// ---- folding the parent's next additions into a frame's combine --------------
-//
-// When the parent schedule continues with a run of additions over blocks of the
-// frame's output shape (std2 rows 13-18 after P1 = A11 B11 -> X: U2 = P1 + P6,
-// U3 = U2 + P7, ...), the combine thread that writes the frame's four output
-// positions runs that dataflow on the same positions right away: one launch and
-// one round trip of the product through HBM fewer.  Every view of the run must
-// be the frame's output itself or disjoint from it, and disjoint from the
-// product planes other threads of the combine still read.
-void post_fold(const Plan& plan, std::size_t oi, double* const base[4], std::vector<char>& folded,
-               Step& comb) {
-    const Op& F = plan.ops[oi];
-    std::size_t j1 = oi + 1;
-    while (j1 < plan.ops.size() && is_add(plan.ops[j1]) && plan.ops[j1].frame == F.frame &&
-           F.frame >= 0 && !folded[j1])
-        ++j1;
-    const std::size_t r = j1 - (oi + 1);
-    if (r == 0) return;
-    auto ok_view = [&](const View& v) {
-        if (v.rows != F.d.rows || v.cols != F.d.cols) return false;
-        if (!v.same_window(F.d) && v.phys_overlaps(F.d)) return false;
-        for (const View* h : {&F.h0, &F.h1, &F.h2})
-            if (h->rows && v.phys_overlaps(*h)) return false;
-        return v.ld % 2 == 0 && v.cols % 2 == 0;
-    };
-    for (std::size_t j = oi + 1; j < j1; ++j) {
-        const Op& o = plan.ops[j];
-        if (!ok_view(o.d) || !ok_view(o.a) || (o.kind == OP_ADDSUB && !ok_view(o.b))) return;
-    }
-    FramePost& Q = comb.fcomb.post;
-    std::memset(&Q, 0, sizeof(Q));
-    const Field& f = plan.field;
-    if (r == 1) {
-        const Op& o = plan.ops[oi + 1];
-        Q.kind = 2;
-        Q.d = base[o.d.region] + o.d.off;
-        Q.a = base[o.a.region] + o.a.off;
-        Q.b = o.kind == OP_ADDSUB ? base[o.b.region] + o.b.off : Q.a;
-        Q.ldd = o.d.ld;
-        Q.lda = o.a.ld;
-        Q.ldb = o.kind == OP_ADDSUB ? o.b.ld : o.a.ld;
-        Q.mode = o.kind == OP_ADDSUB ? modp_add_mode(f, o.sa, o.sb)
-                                     : (f.is_one(o.sa) ? M_COPY : f.is_minus_one(o.sa) ? M_NEG : M_SCALE);
-        Q.sa = static_cast<double>(o.sa.r);
-        Q.sb = static_cast<double>(o.sb.r);
-        if (!aligned16(Q.d) || !aligned16(Q.a) || !aligned16(Q.b)) {
-            Q.kind = 0;
-            return;
-        }
-    } else {
-        const int g = find_group(plan, oi + 1, folded);
-        Step gs{};
-        if (g < 0 || fused::kGroups[g].nins != static_cast<int>(r) ||
-            !try_group(plan, oi + 1, g, base, gs))
-            return;
-        Q.kind = 1;
-        Q.gid = g;
-        Q.g = gs.grp;
-    }
-    for (std::size_t j = oi + 1; j < j1; ++j) {
-        folded[j] = 1;
-        op_sets(plan.ops[j], comb.rd, comb.wr);
-    }
-}
-
 // Lower an operation list to launches.  Additions are merged into one launch
 // while they are pairwise independent (no write of one touches a read or
 // write of another) and contiguous in program order.
@@ -1014,7 +924,7 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             Op fop = op;  // product (and raw) planes in dead blocks when there are some
             View ext[4];
             bool use_ext = false;
-            if (ctx.dead_hosts && !ctx.post_fold && op.frame >= 0) {
+            if (ctx.dead_hosts && op.frame >= 0) {
                 // accumulating frames: a third block takes the raw planes, so that
                 // with two temporaries B22 is materialised too and the GEMM no
                 // longer reads the frame's B (the parent's next prep rewrites it)
@@ -1042,26 +952,12 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 recent_hosts.clear();
                 for (const auto& hv : host_hist) recent_hosts.insert(recent_hosts.end(), hv.begin(), hv.end());
             }
-            lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.frame_cfg,
-                        ctx.direct_ok && ctx.direct_frames, ctx.multicast, ctx.wide_plain,
-                        use_ext ? ext : nullptr);
-            if (ctx.coop_frames && steps.size() == first + 3 && steps[first + 1].engine == 2 &&
-                frame_coop_supported(steps[first + 1].fgemm, steps[first + 1].bn)) {
-                // the three launches as phases of one cooperative launch
-                Step co = steps[first + 1];
-                co.kind = Step::FCOOP;
-                co.fprep = steps[first].fprep;
-                co.fcomb = steps[first + 2].fcomb;
-                steps.resize(first);
-                steps.push_back(co);
-            }
+            lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.direct_ok && ctx.direct_frames,
+                        ctx.wide_plain, use_ext ? ext : nullptr);
             frame_sets(fop, f, steps, first, use_ext ? ext : nullptr);
             if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
                 for (std::size_t j = first; j < steps.size(); ++j)
-                    if (steps[j].kind == Step::FPREP || steps[j].kind == Step::FCOOP)
-                        apply_fold(plan, folds[oi], base, steps[j]);
-            if (ctx.post_fold && !f.real && steps.back().kind == Step::FCOMB)
-                post_fold(plan, oi, base, folded, steps.back());
+                    if (steps[j].kind == Step::FPREP) apply_fold(plan, folds[oi], base, steps[j]);
             continue;
         }
         Step s{};
@@ -1097,7 +993,6 @@ bool long_step(const Step& s) {
         case Step::FPREP: return s.fprep.c >= 1024;
         case Step::FGEMM: return s.fgemm.m >= 1024;
         case Step::FCOMB: return s.fcomb.c >= 1024;
-        case Step::FCOOP: return s.fcomb.c >= 1024;
         default: return false;
     }
 }
@@ -1138,9 +1033,6 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
             else WM_CUDA(launch_gemm_i8(s.fgemm, st));
             break;
         case Step::FCOMB: WM_CUDA(launch_frame_comb(s.fcomb, st)); break;
-        case Step::FCOOP:
-            WM_CUDA(launch_frame_coop(s.fprep, s.fgemm, s.fcomb, *s.tmaps, s.bn, s.bar, st));
-            break;
         case Step::UPLOAD:
             WM_CUDA(cudaMemcpy2DAsync(s.sptr, s.sld * 4, s.hptr, s.hld * 4, s.io_cols * 4, s.io_rows,
                                       cudaMemcpyHostToDevice, st));
@@ -1161,8 +1053,7 @@ void issue(const std::vector<Step>& steps, bool real, cudaStream_t st, int subse
     for (const Step& s : steps) {
         if (subset == 1 && s.kind != Step::ADD && s.kind != Step::GROUP) continue;
         if (subset == 2 && s.kind != Step::MUL) continue;
-        if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB &&
-            s.kind != Step::FCOOP)
+        if (subset == 3 && s.kind != Step::FPREP && s.kind != Step::FGEMM && s.kind != Step::FCOMB)
             continue;
         if (subset == 4 && s.kind != Step::FPREP) continue;
         if (subset == 5 && s.kind != Step::FGEMM) continue;
@@ -1314,7 +1205,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                     r->add_bytes_issued += (s.add.it[i].mode <= M_GEN ? 3 : 2) *
                                            static_cast<std::uint64_t>(s.add.it[i].rows) *
                                            s.add.it[i].cols * sizeof(double);
-            if (s.kind == Step::FGEMM || s.kind == Step::FCOOP) {
+            if (s.kind == Step::FGEMM) {
                 const GemmParams& G = s.fgemm;
                 const std::uint64_t mk = static_cast<std::uint64_t>(G.m) * G.k,
                                     kn = static_cast<std::uint64_t>(G.k) * G.n,
@@ -1325,7 +1216,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                                            kn * (G.b[i].fmt != 0 ? 2 : 8) +
                                            mn * (G.c[i].fmt != 0 ? 2 : 8);
             }
-            if (s.kind == Step::FPREP || s.kind == Step::FCOOP) {
+            if (s.kind == Step::FPREP) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fprep.c) * s.fprep.c;
                 r->frame_bytes += (4 + 4 + 4 + (s.fprep.beta ? 4 : 0)) * c2 * sizeof(double);
                 int planes = 0;
@@ -1337,15 +1228,9 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                         r->frame_prep_bytes += ((ff.s1[0] ? 4 : 0) + (ff.writeback ? 4 : 0)) * c2 *
                                                sizeof(double);
             }
-            if (s.kind == Step::FCOMB || s.kind == Step::FCOOP) {
+            if (s.kind == Step::FCOMB) {
                 const std::uint64_t c2 = static_cast<std::uint64_t>(s.fcomb.c) * s.fcomb.c;
                 r->frame_comb_bytes += 7 * c2 * 2 + (s.fcomb.beta ? c2 * 8 : 0) + 4 * c2 * sizeof(double);
-                const FramePost& Q = s.fcomb.post;  // folded run: slots over 4 c^2 positions
-                if (Q.kind == 1)
-                    r->frame_comb_bytes += static_cast<std::uint64_t>(fused::kGroups[Q.gid].nload +
-                                                                      fused::kGroups[Q.gid].nstore) *
-                                           4 * c2 * sizeof(double);
-                if (Q.kind == 2) r->frame_comb_bytes += 3 * 4 * c2 * sizeof(double);
             }
             if (s.kind == Step::GROUP) {
                 const fused::GroupDesc& G = fused::kGroups[s.gid];
@@ -1469,7 +1354,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->multicast << ctx->fold << ctx->trace << ctx->coop_frames << ctx->stream_io << ctx->post_fold << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << ctx->frame_cfg << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1517,15 +1402,6 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         if (io) {
             const wm_dmat M[3] = {A, B, C};
             add_io_steps(np->steps, *io, M, ctx->f.p);
-        }
-        std::size_t ncoop = 0;
-        for (const Step& st : np->steps) ncoop += st.kind == Step::FCOOP;
-        if (ncoop) {  // zeroed {count, sense} per cooperative launch
-            WM_CUDA(cudaMalloc(&np->bars, 2 * ncoop * sizeof(std::uint32_t)));
-            WM_CUDA(cudaMemset(np->bars, 0, 2 * ncoop * sizeof(std::uint32_t)));
-            std::size_t i = 0;
-            for (Step& st : np->steps)
-                if (st.kind == Step::FCOOP) st.bar = np->bars + 2 * i++;
         }
         ctx->cache.emplace_front(k, std::move(np));
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
@@ -1773,18 +1649,14 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "pdl") g_pdl_user = value != 0;
         else if (k == "prep_rows") g_prep_rows = static_cast<int>(value);
         else if (k == "comb_block") g_comb_block = static_cast<unsigned>(value);
-        else if (k == "multicast") ctx->multicast = value != 0;
         else if (k == "fold") ctx->fold = value != 0;
-        else if (k == "coop_frames") ctx->coop_frames = value != 0;
         else if (k == "stream_io") ctx->stream_io = value != 0;
-        else if (k == "post_fold") ctx->post_fold = value != 0;
         else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "wide_plain") ctx->wide_plain = value != 0;
         else if (k == "cin_direct") ctx->cin_direct = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
-        else if (k == "frame_cfg") ctx->frame_cfg = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
         ctx->cache.clear();
     });
@@ -1804,18 +1676,14 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "pdl") *value = g_pdl_user;
         else if (k == "prep_rows") *value = g_prep_rows;
         else if (k == "comb_block") *value = g_comb_block;
-        else if (k == "multicast") *value = ctx->multicast;
         else if (k == "fold") *value = ctx->fold;
-        else if (k == "coop_frames") *value = ctx->coop_frames;
         else if (k == "stream_io") *value = ctx->stream_io;
-        else if (k == "post_fold") *value = ctx->post_fold;
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;
         else if (k == "cin_direct") *value = ctx->cin_direct;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
-        else if (k == "frame_cfg") *value = ctx->frame_cfg;
         else fail(E_INVALID, "unknown option " + k);
     });
 }
@@ -2007,143 +1875,6 @@ int wm_plan_report_parsed(const char* text, uint32_t p, uint64_t m, uint64_t k, 
     });
 }
 
-// Diagnostics: dependency DAG of a plan's operations (read / write sets by
-// physical overlap).  out[0] = total cost, out[1] = critical-path cost (cost
-// model: fused frame 9, leaf product 6, block addition 2.5 -- microseconds),
-// out[2] = operations, out[3] = critical path in operations.
-int wm_diag_plan_dag(const char* variant, uint64_t m, uint64_t k, uint64_t n, int cutoff,
-                     uint32_t beta, int fuse_frames, double* out) {
-    return guard([&] {
-        Field f;
-        f.p = 65521u;
-        PlanOptions opt;
-        opt.fuse_frames = fuse_frames != 0;
-        Plan plan = plan_variant(variant ? variant : "", f, m, k, n, k, n, n, modp_scalar(f, 1),
-                                 modp_scalar(f, beta), cutoff, opt);
-        const std::size_t N = plan.ops.size();
-        std::vector<std::vector<View>> R(N), Wr(N);
-        std::vector<double> cost(N);
-        for (std::size_t i = 0; i < N; ++i) {
-            const Op& o = plan.ops[i];
-            Wr[i].push_back(o.d);
-            R[i].push_back(o.a);
-            if (o.kind == OP_ADDSUB || o.kind == OP_MUL || o.kind == OP_FRAME) R[i].push_back(o.b);
-            if (o.kind == OP_MUL || o.kind == OP_FRAME) R[i].push_back(o.d);
-            if (o.kind == OP_FRAME) {
-                for (const View* h : {&o.h0, &o.h1, &o.h2})
-                    if (h->rows) Wr[i].push_back(*h);
-            }
-            cost[i] = o.kind == OP_FRAME ? 9.0 : o.kind == OP_MUL ? 6.0 : 2.5;
-        }
-        auto hit = [](const std::vector<View>& x, const std::vector<View>& y) {
-            for (const View& a : x)
-                for (const View& b : y)
-                    if (a.phys_overlaps(b)) return true;
-            return false;
-        };
-        std::vector<double> fin(N, 0.0);
-        std::vector<double> depth(N, 0.0);
-        double total = 0, crit = 0, dcrit = 0;
-        for (std::size_t j = 0; j < N; ++j) {
-            double start = 0, d0 = 0;
-            for (std::size_t i = 0; i < j; ++i) {
-                if (fin[i] <= start && depth[i] <= d0) continue;
-                if (hit(Wr[i], R[j]) || hit(Wr[i], Wr[j]) || hit(R[i], Wr[j])) {
-                    start = std::max(start, fin[i]);
-                    d0 = std::max(d0, depth[i]);
-                }
-            }
-            fin[j] = start + cost[j];
-            depth[j] = d0 + 1;
-            total += cost[j];
-            crit = std::max(crit, fin[j]);
-            dcrit = std::max(dcrit, depth[j]);
-        }
-        out[0] = total;
-        out[1] = crit;
-        out[2] = static_cast<double>(N);
-        out[3] = dcrit;
-        // launch level: lanes of the concurrent issue plan
-        wm_ctx dummy;
-        dummy.gemm_engine = 0;
-        dummy.direct_frames = false;
-        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
-        const std::vector<Step> steps = lower(plan, base, dummy);
-        const DagPlan d = plan_dag(steps, 4);
-        int per_lane[kLanes] = {};  // (4 lanes)
-        std::size_t waits = 0;
-        for (std::size_t j = 0; j < steps.size(); ++j) {
-            ++per_lane[d.lane[j]];
-            waits += d.waits[j].size();
-        }
-        out[4] = static_cast<double>(steps.size());
-        for (int l = 0; l < 4; ++l) out[5 + l] = per_lane[l];
-        out[9] = static_cast<double>(waits);
-        // kinds of the launches off lane 0: ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
-        for (std::size_t j = 0; j < steps.size(); ++j)
-            if (d.lane[j] != 0) out[10 + steps[j].kind] += 1;
-        // launch-level DAG (the read / write sets the concurrent issue uses), cost
-        // model per launch kind in microseconds (measured C2 means):
-        // ADD, MUL, FRAME, GROUP, FPREP, FGEMM, FCOMB
-        const double kc[8] = {2.5, 6.0, 9.0, 2.5, 2.8, 4.1, 2.0, 6.5};
-        const std::size_t S = steps.size();
-        std::vector<double> sfin(S, 0.0);
-        double stot = 0, scrit = 0;
-        for (std::size_t j = 0; j < S; ++j) {
-            double start = 0;
-            for (std::size_t i = j; i-- > 0;) {
-                if (sfin[i] <= start) continue;
-                if (sets_conflict(steps[i], steps[j])) start = std::max(start, sfin[i]);
-            }
-            sfin[j] = start + kc[steps[j].kind];
-            stot += kc[steps[j].kind];
-            scrit = std::max(scrit, sfin[j]);
-        }
-        out[20] = stot;
-        out[21] = scrit;
-        for (const Step& st : steps)
-            if (st.kind == Step::FPREP)
-                for (const FrameFold& ff : st.fprep.fold) {
-                    out[22] += ff.on;
-                    out[23] += ff.on && ff.writeback;
-                }
-        if (std::getenv("WM_DAG_DUMP"))
-            for (std::size_t j = 0; j < steps.size() && j < 400; ++j)
-                std::fprintf(stderr, "%zu lane %d kind %d waits %zu\n", j, d.lane[j], steps[j].kind,
-                             d.waits[j].size());
-    });
-}
-
-// Diagnostics: the launch timeline of the last multiplication run with the
-// "trace" option (concurrent issue only).  Per launch: first CTA start and last
-// CTA end (us after the earliest start; -1 if the kernel has no hook), kind, lane, and up to
-// four launches on other lanes it waits for (-1 padded).  *n = launches.
-int wm_diag_trace(wm_ctx* ctx, int max, double* start_us, double* end_us, int* kind, int* lane,
-                  int* waits, int* n) {
-    return guard([&] {
-        const CachedPlan* cp = nullptr;
-        for (const auto& kv : ctx->cache)
-            if (kv.second.get() == ctx->traced) cp = kv.second.get();
-        if (!cp || !cp->dag) fail(E_INVALID, "no traced multiplication (set trace=1, dag>1)");
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
-        const int N = static_cast<int>(cp->steps.size());
-        *n = N;
-        std::vector<unsigned long long> t(2 * N);
-        WM_CUDA(cudaMemcpy(t.data(), cp->tl, t.size() * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost));
-        unsigned long long t0 = ~0ull;
-        for (int j = 0; j < N; ++j) t0 = std::min(t0, t[2 * j]);
-        for (int j = 0; j < N && j < max; ++j) {
-            start_us[j] = t[2 * j] == ~0ull ? -1.0 : 1e-3 * static_cast<double>(t[2 * j] - t0);
-            end_us[j] = t[2 * j + 1] ? 1e-3 * static_cast<double>(t[2 * j + 1] - t0) : -1.0;
-            kind[j] = cp->steps[j].kind;
-            lane[j] = cp->dag->lane[j];
-            for (int w = 0; w < 4; ++w)
-                waits[4 * j + w] = w < static_cast<int>(cp->dag->waits[j].size()) ? cp->dag->waits[j][w] : -1;
-        }
-    });
-}
-
 int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, int cutoff,
                       wm_report* report) {
     return guard([&] {
@@ -2279,256 +2010,6 @@ int wm_download_u32(wm_ctx* ctx, uint32_t* host, uint64_t host_ld, wm_dmat src) 
     });
 }
 
-// Diagnostics: average microseconds of `reps` back-to-back leaf products
-// C <- A*B (+C) captured as one graph (kernel: 0 DMMA, 1 tcgen05 int8).
-int wm_diag_time_leaf(wm_ctx* ctx, wm_dmat A, wm_dmat B, wm_dmat C, int reps, int kernel,
-                      double* us) {
-    // kernel: 0 DMMA, 1 int8 (auto config), 100*bn + split: int8 forced config
-    return guard([&] {
-        Op op{};
-        op.kind = OP_MUL;
-        op.d = raw_view(C);
-        op.a = raw_view(A);
-        op.b = raw_view(B);
-        op.sa = modp_scalar(ctx->f, 1);
-        op.sb = modp_scalar(ctx->f, 1);
-        double* base[4] = {nullptr, nullptr, nullptr, nullptr};
-        MulParams P = make_mul(op, ctx->f, base);
-        if (kernel >= 1 && !leaf_i8_supported(P)) fail(E_INVALID, "shape unsupported by i8 leaf");
-        cudaGraph_t g;
-        cudaGraphExec_t ge;
-        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < reps; ++i) {
-            cudaError_t e;
-            if (kernel >= 10000) {  // TMA engine, forced (bn, split)
-                GemmParams G = gemm_from_mul(P);
-                static TmaMaps M;
-                const int bn = (kernel - 10000) / 100, sp = kernel % 100;
-                e = gemm_tma_encode(G, bn, M) ? launch_gemm_tma(G, M, bn, sp, ctx->stream)
-                                              : cudaErrorInvalidValue;
-            } else if (kernel == 2) {  // TMA engine, automatic tiling
-                GemmParams G = gemm_from_mul(P);
-                static TmaMaps M;
-                int bn, sp;
-                gemm_choose(G, &bn, &sp);
-                e = gemm_tma_encode(G, bn, M) ? launch_gemm_tma(G, M, bn, sp, ctx->stream)
-                                              : cudaErrorInvalidValue;
-            } else if (kernel == 1) {
-                e = launch_leaf_i8(P, ctx->stream);
-            } else if (kernel > 2) {
-                e = launch_leaf_i8_cfg(P, kernel / 100, kernel % 100, ctx->stream);
-            } else {
-                e = launch_leaf_dmma(P, ctx->f.real, ctx->stream);
-            }
-            if (e != cudaSuccess) {
-                cudaGraph_t g2;
-                cudaStreamEndCapture(ctx->stream, &g2);
-                if (g2) cudaGraphDestroy(g2);
-                fail(E_INVALID, "leaf config rejected");
-            }
-        }
-        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, ctx->stream);
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEventRecord(e1, ctx->stream);
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        *us = 1000.0 * ms / reps;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
-    });
-}
-
-// Diagnostics: the seven-product frame GEMM on uint16 planes of a c x c frame,
-// forced tiling cfg (100*bn + split; 0 = automatic), timed over `reps` graph-
-// replayed launches; trace_out (optional, 16 x #CTAs u64) gets one traced launch.
-int wm_diag_frame_gemm(wm_ctx* ctx, uint32_t c, int cfg, int reps, double* us,
-                       unsigned long long* trace_out, int* nctas) {
-    return guard([&] {
-        const std::size_t plane = static_cast<std::size_t>(c) * c;
-        std::uint16_t* buf = nullptr;
-        WM_CUDA(cudaMalloc(&buf, 21 * plane * sizeof(std::uint16_t)));
-        WM_CUDA(cudaMemset(buf, 1, 21 * plane * sizeof(std::uint16_t)));
-        GemmParams G{};
-        for (int k = 0; k < 7; ++k) {
-            G.a[k] = {buf + (3 * k) * plane, c, 1};
-            G.b[k] = {buf + (3 * k + 1) * plane, c, 1};
-            G.c[k] = {buf + (3 * k + 2) * plane, c, 1};
-        }
-        G.m = G.n = G.k = c;
-        G.nprod = 7;
-        G.tiles_m = c / 128;
-        G.alpha = 1;
-        G.pd = static_cast<double>(ctx->f.p);
-        G.pinv = 1.0 / G.pd;
-        Step st{};
-        st.fgemm = G;
-        finish_gemm_step(st, 1, cfg);
-        if (st.engine != 1) fail(E_INVALID, "TMA engine unavailable");
-        *nctas = st.split * static_cast<int>(G.n / st.bn) * static_cast<int>(G.tiles_m * 7);
-        cudaGraph_t g;
-        cudaGraphExec_t ge;
-        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < reps; ++i) launch_gemm_tma(st.fgemm, *st.tmaps, st.bn, st.split, ctx->stream);
-        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        cudaEventRecord(e0, ctx->stream);
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEventRecord(e1, ctx->stream);
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        *us = 1000.0 * ms / reps;
-        if (trace_out) {
-            unsigned long long* dtr = nullptr;
-            const std::size_t n = static_cast<std::size_t>(*nctas) * 16;
-            WM_CUDA(cudaMalloc(&dtr, n * sizeof(unsigned long long)));
-            WM_CUDA(cudaMemset(dtr, 0, n * sizeof(unsigned long long)));
-            st.fgemm.trace = dtr;
-            WM_CUDA(launch_gemm_tma(st.fgemm, *st.tmaps, st.bn, st.split, ctx->stream));
-            WM_CUDA(cudaStreamSynchronize(ctx->stream));
-            WM_CUDA(cudaMemcpy(trace_out, dtr, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-            cudaFree(dtr);
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
-        cudaFree(buf);
-    });
-}
-
-// Diagnostics: seven c x c x c products on random limb planes through the
-// direct-limb engine (product 2 with a float64 B when bconv), checked on the host.
-int wm_diag_direct_check(wm_ctx* ctx, uint32_t c, int bn, int bconv, uint64_t seed,
-                         uint64_t* mismatches, double* us, unsigned long long* trace_out) {
-    return guard([&] {
-        if (!ctx->direct_ok) fail(E_INVALID, "direct engine unavailable");
-        const std::uint64_t p = ctx->f.p, pitch = 2ull * c + 128, cc = static_cast<std::uint64_t>(c) * c;
-        std::vector<std::uint16_t> A(7 * cc), B(7 * cc);
-        std::uint64_t x = seed;
-        auto next = [&]() {
-            std::uint64_t z = (x += 0x9E3779B97F4A7C15ull);
-            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-            z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-            return static_cast<std::uint16_t>((z ^ (z >> 31)) % p);
-        };
-        for (auto& v : A) v = next();
-        for (auto& v : B) v = next();
-        std::vector<std::uint8_t> pa(7 * c * pitch, 0), pb(7 * c * pitch, 0);
-        for (int k = 0; k < 7; ++k)
-            for (std::uint64_t r = 0; r < c; ++r)
-                for (std::uint64_t j = 0; j < c; ++j) {
-                    const std::uint16_t a = A[k * cc + r * c + j], b = B[k * cc + r * c + j];
-                    std::uint8_t* ra = pa.data() + (k * c + r) * pitch;
-                    std::uint8_t* rb = pb.data() + (k * c + r) * pitch;
-                    ra[j] = static_cast<std::uint8_t>(a >> 8);
-                    ra[c + j] = static_cast<std::uint8_t>(a & 255);
-                    rb[j] = static_cast<std::uint8_t>(b >> 8);
-                    rb[c + j] = static_cast<std::uint8_t>(b & 255);
-                }
-        std::vector<double> bf(cc);
-        for (std::uint64_t i = 0; i < cc; ++i) bf[i] = B[2 * cc + i];
-        std::uint8_t *da = nullptr, *db = nullptr;
-        double* dbf = nullptr;
-        std::uint16_t* dout = nullptr;
-        WM_CUDA(cudaMalloc(&da, pa.size()));
-        WM_CUDA(cudaMalloc(&db, pb.size()));
-        WM_CUDA(cudaMalloc(&dbf, cc * sizeof(double)));
-        WM_CUDA(cudaMalloc(&dout, 7 * cc * sizeof(std::uint16_t)));
-        WM_CUDA(cudaMemcpy(da, pa.data(), pa.size(), cudaMemcpyHostToDevice));
-        WM_CUDA(cudaMemcpy(db, pb.data(), pb.size(), cudaMemcpyHostToDevice));
-        WM_CUDA(cudaMemcpy(dbf, bf.data(), cc * sizeof(double), cudaMemcpyHostToDevice));
-        WM_CUDA(cudaMemset(dout, 0xFF, 7 * cc * sizeof(std::uint16_t)));
-        GemmParams G{};
-        for (int k = 0; k < 7; ++k) {
-            G.a[k] = {da + k * c * pitch, pitch, 2, c};
-            G.b[k] = (bconv && k == 2) ? GemmSrc{dbf, c, 0, 0} : GemmSrc{db + k * c * pitch, pitch, 2, c};
-            G.c[k] = {dout + k * cc, c, 1, 0};
-        }
-        G.m = G.n = G.k = c;
-        G.nprod = 7;
-        G.tiles_m = c / 128;
-        G.alpha = 1;
-        G.pd = static_cast<double>(p);
-        G.pinv = 1.0 / G.pd;
-        const bool mcast = bn >= 10000;
-        bn %= 10000;
-        gemm_direct_cluster(G, bn, mcast);
-        if (!gemm_direct_supported(G, bn)) fail(E_INVALID, "direct engine: unsupported shape");
-        TmaMaps M;
-        if (!gemm_direct_encode(G, bn, M)) fail(E_INVALID, "direct engine: tensor map encode failed");
-        WM_CUDA(launch_gemm_direct(G, M, bn, ctx->stream));
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
-        cudaEvent_t e0, e1;
-        cudaEventCreate(&e0);
-        cudaEventCreate(&e1);
-        const int reps = 20;
-        cudaGraph_t g;
-        cudaGraphExec_t ge;
-        WM_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < reps; ++i) launch_gemm_direct(G, M, bn, ctx->stream);
-        WM_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-        WM_CUDA(cudaGraphInstantiate(&ge, g, 0));
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEventRecord(e0, ctx->stream);
-        WM_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        cudaEventRecord(e1, ctx->stream);
-        WM_CUDA(cudaStreamSynchronize(ctx->stream));
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        *us = 1000.0 * ms / reps;
-        if (trace_out) {
-            const std::size_t n = static_cast<std::size_t>(G.tiles_m) * 7 * (c / (bn % 1000)) * 16;
-            unsigned long long* dtr = nullptr;
-            WM_CUDA(cudaMalloc(&dtr, n * sizeof(unsigned long long)));
-            WM_CUDA(cudaMemset(dtr, 0, n * sizeof(unsigned long long)));
-            G.trace = dtr;
-            WM_CUDA(launch_gemm_direct(G, M, bn, ctx->stream));
-            WM_CUDA(cudaStreamSynchronize(ctx->stream));
-            G.trace = nullptr;
-            WM_CUDA(cudaMemcpy(trace_out, dtr, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-            cudaFree(dtr);
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-        std::vector<std::uint16_t> out(7 * cc);
-        WM_CUDA(cudaMemcpy(out.data(), dout, out.size() * 2, cudaMemcpyDeviceToHost));
-        cudaFree(da);
-        cudaFree(db);
-        cudaFree(dbf);
-        cudaFree(dout);
-        std::uint64_t bad = 0;
-        std::vector<std::uint64_t> acc(c);
-        for (int k = 0; k < 7; ++k)
-            for (std::uint64_t i = 0; i < c; ++i) {
-                std::fill(acc.begin(), acc.end(), 0);
-                for (std::uint64_t t = 0; t < c; ++t) {
-                    const std::uint64_t a = A[k * cc + i * c + t];
-                    const std::uint16_t* brow = &B[k * cc + t * c];
-                    for (std::uint64_t j = 0; j < c; ++j) acc[j] += a * brow[j];
-                }
-                for (std::uint64_t j = 0; j < c; ++j)
-                    if (out[k * cc + i * c + j] != acc[j] % p) ++bad;
-            }
-        *mismatches = bad;
-    });
-}
-
 uint64_t wm_fnv1a64_u32(const uint32_t* data, uint64_t count) {
     std::uint64_t h = 0xcbf29ce484222325ull;
     for (std::uint64_t i = 0; i < count; ++i) {
@@ -2545,5 +2026,9 @@ int wm_fill_random(wm_ctx* ctx, wm_dmat dst, uint64_t seed) {
                                      ctx->f.real, ctx->stream));
     });
 }
+
+#if WM_DIAG  // measurement-only exports: libwinomem_b200_diag.so (build.py)
+#include "wm_runtime_diag.inc"
+#endif
 
 }  // extern "C"

@@ -181,12 +181,15 @@ def main():
     w("    double p, pinv;")
     w("};")
     w("")
+    w("// lazy modular reduction (wm_apply.cuh): a run's intermediate values stay")
+    w("// unreduced (exact integers in float64); every stored slot is canonicalised once")
     w("template <bool REAL>")
-    w("__device__ __forceinline__ double gop(std::uint32_t mode, double a, double b, double sa,")
+    w("__device__ __forceinline__ double lop(std::uint32_t mode, double a, double b, double sa,")
     w("                                      double sb, double p, double pinv);")
+    w("template <bool REAL>")
+    w("__device__ __forceinline__ double canon(double v, double p, double pinv);")
     w("")
-    w("// LDG: read-only path for slots nothing in the kernel writes; plain loads when")
-    w("// the run is folded behind a frame combine that just wrote one of its slots")
+    w("// LDG: read-only path for slots nothing in the kernel writes")
     w("template <bool LDG>")
     w("__device__ __forceinline__ double2 gld(const double* p) {")
     w("    return LDG ? __ldg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);")
@@ -208,57 +211,15 @@ def main():
         for j, (_, kind, dst, ops) in enumerate(g["run"]):
             d, a = idx[dst], idx[ops[0]]
             b = idx[ops[1]] if kind == "add" else a
-            w(f"    s{d} = make_double2(gop<REAL>(G.mode[{j}], s{a}.x, s{b}.x, G.sa[{j}], "
-              f"G.sb[{j}], G.p, G.pinv), gop<REAL>(G.mode[{j}], s{a}.y, s{b}.y, G.sa[{j}], "
+            w(f"    s{d} = make_double2(lop<REAL>(G.mode[{j}], s{a}.x, s{b}.x, G.sa[{j}], "
+              f"G.sb[{j}], G.p, G.pinv), lop<REAL>(G.mode[{j}], s{a}.y, s{b}.y, G.sa[{j}], "
               f"G.sb[{j}], G.p, G.pinv));")
         for s in g["stores"]:
             i = idx[s]
-            w(f"    *reinterpret_cast<double2*>(G.v[{i}] + r * G.ld[{i}] + c) = s{i};")
+            w(f"    *reinterpret_cast<double2*>(G.v[{i}] + r * G.ld[{i}] + c) = "
+              f"make_double2(canon<REAL>(s{i}.x, G.p, G.pinv), canon<REAL>(s{i}.y, G.p, G.pinv));")
         w("}")
         w("")
-    # four positions per call, every load issued before any store: the frame
-    # combine runs a folded run on the four output positions of one thread
-    for gi, g in enumerate(groups):
-        idx = {s: i for i, s in enumerate(g["slots"])}
-        w("template <bool REAL>")
-        w(f"__device__ __forceinline__ void group_body4_{gi}(const GroupParams& G, const std::uint64_t* r,"
-          " const std::uint64_t* c) {")
-        for s in g["loads"]:
-            i = idx[s]
-            w(f"    double2 s{i}[4];")
-        w("#pragma unroll")
-        w("    for (int q = 0; q < 4; ++q) {")
-        for s in g["loads"]:
-            i = idx[s]
-            w(f"        s{i}[q] = *reinterpret_cast<const double2*>(G.v[{i}] + r[q] * G.ld[{i}] + c[q]);")
-        w("    }")
-        for s in g["slots"]:
-            if s not in g["loads"]:
-                w(f"    double2 s{idx[s]}[4];")
-        w("#pragma unroll")
-        w("    for (int q = 0; q < 4; ++q) {")
-        for j, (_, kind, dst, ops) in enumerate(g["run"]):
-            d, a = idx[dst], idx[ops[0]]
-            b = idx[ops[1]] if kind == "add" else a
-            w(f"        s{d}[q] = make_double2(gop<REAL>(G.mode[{j}], s{a}[q].x, s{b}[q].x, G.sa[{j}], "
-              f"G.sb[{j}], G.p, G.pinv), gop<REAL>(G.mode[{j}], s{a}[q].y, s{b}[q].y, G.sa[{j}], "
-              f"G.sb[{j}], G.p, G.pinv));")
-        for s in g["stores"]:
-            i = idx[s]
-            w(f"        *reinterpret_cast<double2*>(G.v[{i}] + r[q] * G.ld[{i}] + c[q]) = s{i}[q];")
-        w("    }")
-        w("}")
-        w("")
-    w("template <bool REAL>")
-    w("__device__ __forceinline__ void group_dispatch4(int gid, const GroupParams& G,"
-      " const std::uint64_t* r, const std::uint64_t* c) {")
-    w("    switch (gid) {")
-    for gi in range(len(groups)):
-        w(f"        case {gi}: group_body4_{gi}<REAL>(G, r, c); break;")
-    w("        default: break;")
-    w("    }")
-    w("}")
-    w("")
     w("template <bool REAL, bool LDG = true>")
     w("__device__ __forceinline__ void group_dispatch(int gid, const GroupParams& G,"
       " std::uint64_t r, std::uint64_t c) {")

@@ -1,4 +1,5 @@
 """Direct-limb frame GEMM: correctness (host check) and timing per shape."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import json
 

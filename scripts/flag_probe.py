@@ -1,4 +1,5 @@
 """Dependent-launch floor: griddepcontrol.wait (PDL) vs a counter handoff."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import os
 import sys

@@ -1,4 +1,5 @@
 """Seven-product frame GEMM in isolation: tiling sweep + per-CTA phase trace."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import json
 import os

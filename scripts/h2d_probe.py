@@ -1,4 +1,5 @@
 """Pinned host -> device copy rate: contiguous vs quadrant 2-D copies."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import os
 import sys

@@ -1,4 +1,5 @@
 """Run one leaf product size a few times (for ncu captures)."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import os
 import sys

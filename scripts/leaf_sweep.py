@@ -1,4 +1,5 @@
 """Sweep int8 leaf configurations (BN, K-split) per leaf size; graph-replayed."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import json
 import os

@@ -1,6 +1,7 @@
 """Calibration microbenchmarks on the B200 (design inputs, not the bench):
 launch latency, per-SM / chip streaming bandwidth, leaf GEMM rates (DMMA vs
 tcgen05 int8 limbs) at the leaf sizes of the BASELINE configs."""
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import json
 import os

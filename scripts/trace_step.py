@@ -3,6 +3,7 @@ concurrent issue) and its critical path, attributed per launch kind.
 
     python scripts/trace_step.py [C2]
 """
+import os; os.environ.setdefault("WM_DIAG", "1")  # the wm_diag_* probes live in the diag library  # noqa: E702,E401
 import ctypes as C
 import json
 import os

@@ -43,16 +43,15 @@ def golden():
 
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
                         dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
-                        dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0), dict(multicast=1),
-                        dict(fold=0), dict(coop_frames=1), dict(coop_frames=0), dict(post_fold=1), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0)],
+                        dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0),
+                        dict(fold=0), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0)],
                 ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync", "convert-frames",
-                     "one-stream", "multicast", "no-fold", "coop", "no-coop", "post-fold", "no-dead-hosts", "narrow-plain", "packed-cin"])
+                     "one-stream", "no-fold", "no-dead-hosts", "narrow-plain", "packed-cin"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
                                               "leaf_kernel", "fuse_adds", "gemm_engine",
-                                              "direct_frames", "dag", "multicast", "fold",
-                                              "coop_frames", "post_fold", "dead_hosts",
+                                              "direct_frames", "dag", "fold", "dead_hosts",
                                               "wide_plain", "cin_direct")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
@@ -230,15 +229,20 @@ def test_direct_limb_gemm(W, c, bn, bconv):
     with a float64 B), every residue checked on the host (wm_diag_direct_check)."""
     import ctypes as C
     from paper_0707_2347_b200 import _lib
-    L = _lib.lib()
+    L = _lib.diag_lib()  # the kernel-level checker lives in the diagnostics build
     f = L.wm_diag_direct_check
     f.argtypes = [C.c_void_p, C.c_uint32, C.c_int, C.c_int, C.c_uint64,
                   C.POINTER(C.c_uint64), C.POINTER(C.c_double), C.c_void_p]
     f.restype = C.c_int
-    bad, us = C.c_uint64(), C.c_double()
-    rc = f(W.Context.get().h, c, bn, bconv, 1000 + c + bn, C.byref(bad), C.byref(us), None)
-    assert rc == 0, _lib.last_error() if hasattr(_lib, "last_error") else rc
-    assert bad.value == 0
+    h = C.c_void_p()
+    assert L.wm_ctx_create(0, 65521, 0, None, C.byref(h)) == 0, L.wm_last_error()
+    try:
+        bad, us = C.c_uint64(), C.c_double()
+        rc = f(h, c, bn, bconv, 1000 + c + bn, C.byref(bad), C.byref(us), None)
+        assert rc == 0, L.wm_last_error()
+        assert bad.value == 0
+    finally:
+        L.wm_ctx_destroy(h)
 
 
 def test_host_u32_end_to_end(W, O):
