@@ -102,6 +102,10 @@ const char* wm_last_error(void);
 int wm_ctx_create(int device, uint32_t p, int field, void* stream, wm_ctx** out);
 int wm_ctx_destroy(wm_ctx* ctx);
 int wm_ctx_sync(wm_ctx* ctx);
+/* the context's device, modulus, field and current stream (cudaStream_t) */
+int wm_ctx_info(wm_ctx* ctx, int* device, uint32_t* p, int* field, void** stream);
+/* issue subsequent work on `stream` (a cudaStream_t of the same device) */
+int wm_ctx_set_stream(wm_ctx* ctx, void* stream);
 /* options (defaults in brackets; every change drops the cached plans):
  *   "fuse_frames" [1]   fused leaf frames (prep / seven-product GEMM / combine)
  *   "graphs" [1]        capture each plan once into a CUDA graph
@@ -153,6 +157,33 @@ int wm_run_variant_real(wm_ctx* ctx, const char* variant, wm_dmat A, wm_dmat B, 
 int wm_run_variant_host_u32(wm_ctx* ctx, const char* variant, uint64_t m, uint64_t k, uint64_t n,
                             uint32_t* A, uint32_t* B, uint32_t* C, uint32_t alpha, uint32_t beta,
                             int cutoff, wm_report* report);
+
+/* ---- multi-GPU product partition (wm_dist.cpp) -------------
+ * run_variant (drivers.hpp:213-222) with the 7^L products of the top L Winograd
+ * levels spread over the ranks of an NCCL communicator (product t on rank
+ * t mod G): the root broadcasts A and B, every rank forms its own operands and
+ * multiplies them with the single-GPU plan, products return to the root, which
+ * folds alpha*coef*P into C (after C <- beta*C).  One process or thread per GPU;
+ * NCCL is loaded at run time (libnccl.so.2).  wm_dist_unique_id runs on rank 0
+ * and the caller ships the 128 bytes to the other ranks.  On ranks != 0 pass
+ * empty A, B, C (their shapes come from the root).  levels 0: chosen by the
+ * makespan bound (wm_dist_choose_levels); window: receive buffers on the root. */
+typedef struct wm_dist wm_dist;
+typedef struct {
+    int levels;
+    uint64_t products;          /* products this rank computed */
+    uint64_t peak_extra_bytes;  /* device bytes this rank held at once (operand copies, */
+                                /* operands, products, receive ring, local plan temporaries) */
+    uint64_t bytes_sent, bytes_received;
+} wm_dist_report;
+int wm_dist_unique_id(unsigned char id[128]);
+int wm_dist_create(wm_ctx* ctx, int rank, int world, const unsigned char id[128], wm_dist** out);
+int wm_dist_destroy(wm_dist* d);
+int wm_dist_choose_levels(int world, uint64_t n, int cutoff);
+int wm_dist_run_variant(wm_dist* d, const char* variant, wm_dmat A, wm_dmat B, wm_dmat C,
+                        uint32_t alpha, uint32_t beta, int cutoff, int levels, int window,
+                        wm_dist_report* report);
+const char* wm_dist_last_error(void);
 
 /* ---- host-only planning (no device needed) --------------------------------- */
 /* Plans `variant` and returns the exact CostReport the reference meter would

@@ -15,4 +15,4 @@ from .winomem import (  # noqa: F401
     partial_overlap_error, plan_report, quad_split, render_schedule, run_parsed_schedule,
     run_variant, run_variant_host, shape_error, unknown_schedule_error, unknown_slot_error,
     variant_accumulates, workspace_error, io_error, matrix_file_info, read_matrix_host,
-    write_matrix_host, read_text, read_binary, write_text, write_binary, lincomb)
+    write_matrix_host, read_text, read_binary, write_text, write_binary, lincomb, DistContext)

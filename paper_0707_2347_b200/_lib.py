@@ -30,13 +30,20 @@ EXPORTS = [
     "wm_run_parsed_schedule", "wm_parse_schedule", "wm_render_schedule",
     "wm_run_parsed_schedule_host_u32", "wm_matrix_file_info", "wm_matrix_read_host",
     "wm_matrix_write_host", "wm_matrix_read_device", "wm_matrix_write_device",
-    "wm_plan_report_parsed", "wm_lincomb", "wm_dev_alloc", "wm_dev_free",
+    "wm_plan_report_parsed", "wm_lincomb", "wm_dev_alloc", "wm_dev_free", "wm_ctx_info",
+    "wm_ctx_set_stream", "wm_dist_unique_id", "wm_dist_create", "wm_dist_destroy",
+    "wm_dist_choose_levels", "wm_dist_run_variant", "wm_dist_last_error",
 ]
 
 
 class wm_dmat(C.Structure):
     _fields_ = [("ptr", C.c_void_p), ("rows", C.c_uint64), ("cols", C.c_uint64),
                 ("ld", C.c_uint64)]
+
+
+class wm_dist_report(C.Structure):
+    _fields_ = [("levels", C.c_int), ("products", C.c_uint64), ("peak_extra_bytes", C.c_uint64),
+                ("bytes_sent", C.c_uint64), ("bytes_received", C.c_uint64)]
 
 
 class wm_report(C.Structure):
@@ -102,6 +109,15 @@ def lib():
     L.wm_run_parsed_schedule_host_u32.argtypes = [ctx_p, C.c_char_p, u64, u64, u64, C.c_void_p,
                                                   C.c_void_p, C.c_void_p, u32, u32, i32,
                                                   P(wm_report)]
+    L.wm_ctx_info.argtypes = [ctx_p, P(i32), P(u32), P(i32), P(C.c_void_p)]
+    L.wm_ctx_set_stream.argtypes = [ctx_p, C.c_void_p]
+    L.wm_dist_unique_id.argtypes = [C.c_char_p]
+    L.wm_dist_create.argtypes = [ctx_p, i32, i32, C.c_char_p, P(C.c_void_p)]
+    L.wm_dist_destroy.argtypes = [C.c_void_p]
+    L.wm_dist_choose_levels.argtypes = [i32, u64, i32]
+    L.wm_dist_run_variant.argtypes = [C.c_void_p, C.c_char_p, wm_dmat, wm_dmat, wm_dmat, u32, u32,
+                                      i32, i32, i32, P(wm_dist_report)]
+    L.wm_dist_last_error.restype = C.c_char_p
     _lib = L
     return L
 

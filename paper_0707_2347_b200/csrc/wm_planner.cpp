@@ -576,6 +576,14 @@ Plan plan_variant(const std::string& variant, Field f, std::uint64_t m, std::uin
     ctx.meter = &plan.meter;
     ctx.ws = &heap;
     ctx.out = &plan.ops;
+    {  // unit-size recursions emit ~10^5-10^6 operations: reserve instead of regrowing
+        std::uint64_t side = std::min({m, k, n}), leaves = 1;
+        while (side > static_cast<std::uint64_t>(std::max(cutoff, 1)) && leaves < (1u << 22)) {
+            side /= 2;
+            leaves *= 7;
+        }
+        plan.ops.reserve(static_cast<std::size_t>(4 * leaves));
+    }
     ctx.opt = &opt;
     int frame_counter = 0;
     ctx.frame_counter = &frame_counter;

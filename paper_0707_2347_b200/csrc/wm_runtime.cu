@@ -29,6 +29,7 @@
 #include "wm_fused.h"
 #include "wm_gemm.h"
 #include "wm_launch.h"
+#include "wm_micro.h"
 #include "wm_planner.h"
 
 namespace wm {
@@ -164,8 +165,13 @@ struct CachedPlan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     unsigned long long* tl = nullptr;  // measurement timeline (trace option)
+    MicroOp* micro = nullptr;          // tiny plans: the whole op list for one launch (wm_micro.cu)
+    std::uint32_t micro_n = 0;
+    MicroImage micro_img{};            // its shared-memory working set
+    bool micro_small = false;          // every operation small: one warp walks it
     ~CachedPlan() {
         if (tl) cudaFree(tl);
+        if (micro) cudaFree(micro);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
         if (arena) cudaFree(arena);
@@ -208,6 +214,7 @@ struct wm_ctx {
                                 // measured: 3 >= 2, 4 > 8 lanes)
     bool fold = true;           // fold a frame's operand-producing additions into its prep
     bool stream_io = true;      // host u32 boundary as quadrant copy steps inside the graph
+    bool micro = true;          // plans of tiny operations as one micro launch (wm_micro.cu)
     bool dead_hosts = true;     // frame product planes in dead blocks (choose_product_hosts)
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
@@ -1341,6 +1348,74 @@ void add_io_steps(std::vector<Step>& steps, const HostIO& io, const wm_dmat M[3]
     steps.swap(out);
 }
 
+// A plan whose every operation is tiny (the unit-size recursions of the
+// reference's test shapes) runs as ONE micro launch over its operation list
+// (wm_micro.cu) instead of one launch per operation.
+bool micro_plan(const wm_ctx& ctx, const Plan& plan, double* const base[4], CachedPlan& cp,
+                const wm_dmat& A, const wm_dmat& B, const wm_dmat& C) {
+    if (!ctx.micro || ctx.f.real || ctx.subset || ctx.trace || plan.ops.empty()) return false;
+    for (const Op& op : plan.ops) {
+        if (op.kind == OP_FRAME || op.d.words() > kMicroMaxWords) return false;
+        if (op.kind == OP_MUL && op.a.rows * op.a.cols * op.b.cols > kMicroMaxLeafVolume) return false;
+    }
+    // stage the working set in shared memory when it fits: operands then carry
+    // byte offsets into the image instead of addresses
+    MicroImage& img = cp.micro_img;
+    img = MicroImage{};
+    const std::uint64_t shape[4][3] = {{A.rows, A.cols, A.ld}, {B.rows, B.cols, B.ld},
+                                       {C.rows, C.cols, C.ld}, {1, plan.arena_words, plan.arena_words}};
+    std::uint64_t words = 0;
+    for (int r = 0; r < 4; ++r) {
+        if (!shape[r][1]) continue;
+        MicroRegion& R = img.region[img.nregions++];
+        R = {base[r], shape[r][0], shape[r][1], shape[r][2], words, r < 3 ? 1 : 0, r < 3 ? 1 : 0};
+        words += shape[r][0] * shape[r][2];
+    }
+    img.words = words;
+    double* off[4] = {nullptr, nullptr, nullptr, nullptr};
+    const bool smem = words * sizeof(double) <= micro_smem_limit();
+    if (smem) {
+        int i = 0;
+        for (int r = 0; r < 4; ++r)
+            if (shape[r][1]) off[r] = reinterpret_cast<double*>(img.region[i++].offset * sizeof(double));
+    } else {
+        img.nregions = 0;
+    }
+    double* const* addr = smem ? off : base;
+    std::vector<MicroOp> ops;
+    ops.reserve(plan.ops.size());
+    bool small = true;
+    for (const Op& op : plan.ops) {
+        MicroOp m{};
+        if (op.kind == OP_MUL) {
+            const MulParams P = make_mul(op, ctx.f, addr);
+            m.d = P.C, m.a = P.A, m.b = P.B;
+            m.ldd = static_cast<std::uint32_t>(P.ldc), m.lda = static_cast<std::uint32_t>(P.lda);
+            m.ldb = static_cast<std::uint32_t>(P.ldb);
+            m.rows = P.m, m.cols = P.n, m.k = P.k;
+            m.kind = MicroOp::MUL;
+            m.sa = P.alpha, m.sb = P.beta;
+            small = small && static_cast<std::uint64_t>(P.m) * P.n * P.k <= kMicroSmallLeafVolume;
+        } else {
+            const AddItem t = make_item(op, ctx.f, addr);
+            m.d = t.d, m.a = t.a, m.b = t.b;
+            m.ldd = static_cast<std::uint32_t>(t.ldd), m.lda = static_cast<std::uint32_t>(t.lda);
+            m.ldb = static_cast<std::uint32_t>(t.ldb);
+            m.rows = t.rows, m.cols = t.cols;
+            m.kind = MicroOp::ADD;
+            m.mode = t.mode, m.sa = t.sa, m.sb = t.sb;
+            small = small && static_cast<std::uint64_t>(t.rows) * t.cols <= kMicroSmallWords;
+        }
+        m.csh = (m.cols & (m.cols - 1)) == 0 ? static_cast<std::uint32_t>(__builtin_ctz(m.cols)) : 0xFFu;
+        ops.push_back(m);
+    }
+    WM_CUDA(cudaMalloc(&cp.micro, ops.size() * sizeof(MicroOp)));
+    WM_CUDA(cudaMemcpy(cp.micro, ops.data(), ops.size() * sizeof(MicroOp), cudaMemcpyHostToDevice));
+    cp.micro_n = static_cast<std::uint32_t>(ops.size());
+    cp.micro_small = small;
+    return true;
+}
+
 void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dmat& B,
          const wm_dmat& C, Scalar alpha, Scalar beta, int cutoff, wm_report* rep,
          const Schedule* parsed = nullptr, const HostIO* io = nullptr) {
@@ -1354,7 +1429,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->micro << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1381,7 +1456,9 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         if (np->plan.arena_words)
             WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
         double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
-        try {
+        if (!io && micro_plan(*ctx, np->plan, base, *np, A, B, C)) {
+            // tiny plan: nothing to lower
+        } else try {
             np->steps = lower(np->plan, base, *ctx);
         } catch (const Error& e) {
             // a frame GEMM the tensor-map path cannot describe: plan again with
@@ -1406,6 +1483,13 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         ctx->cache.emplace_front(k, std::move(np));
         while (ctx->cache.size() > 8) ctx->cache.pop_back();
         cp = ctx->cache.front().second.get();
+    }
+    if (cp->micro) {
+        WM_CUDA(launch_micro(cp->micro, cp->micro_n, cp->micro_img, cp->micro_small, ctx->f.p,
+                             ctx->stream));
+        fill_report(cp->plan, nullptr, rep);
+        if (rep) rep->n_launches = 1;
+        return;
     }
     // concurrent issue pays only for launches of real size; tiny problems (deep
     // recursions of the unit tests) would spend more on the dependency analysis
@@ -1635,6 +1719,23 @@ int wm_ctx_sync(wm_ctx* ctx) {
     return guard([&] { WM_CUDA(cudaStreamSynchronize(ctx->stream)); });
 }
 
+int wm_ctx_info(wm_ctx* ctx, int* device, uint32_t* p, int* field, void** stream) {
+    return guard([&] {
+        if (!ctx) fail(E_INVALID, "null context");
+        if (device) *device = ctx->device;
+        if (p) *p = ctx->f.p;
+        if (field) *field = ctx->f.real ? WM_FIELD_REAL64 : WM_FIELD_MODP;
+        if (stream) *stream = ctx->stream;
+    });
+}
+
+int wm_ctx_set_stream(wm_ctx* ctx, void* stream) {
+    return guard([&] {
+        if (!ctx || !stream) fail(E_INVALID, "null context or stream");
+        ctx->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
 int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
     return guard([&] {
         const std::string k = key ? key : "";
@@ -1651,6 +1752,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "comb_block") g_comb_block = static_cast<unsigned>(value);
         else if (k == "fold") ctx->fold = value != 0;
         else if (k == "stream_io") ctx->stream_io = value != 0;
+        else if (k == "micro") ctx->micro = value != 0;
         else if (k == "dead_hosts") ctx->dead_hosts = value != 0;
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "wide_plain") ctx->wide_plain = value != 0;
@@ -1678,6 +1780,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "comb_block") *value = g_comb_block;
         else if (k == "fold") *value = ctx->fold;
         else if (k == "stream_io") *value = ctx->stream_io;
+        else if (k == "micro") *value = ctx->micro;
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;

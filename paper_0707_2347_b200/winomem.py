@@ -604,3 +604,46 @@ def variant_accumulates(v):
     if v not in BUILTIN_NAMES:
         raise unknown_schedule_error("unknown schedule: " + v)
     return v in _ACC
+
+
+# ---- multi-GPU product partition through the C-ABI (wm_dist_*) ----------------
+class DistContext:
+    """wm_dist_create / wm_dist_run_variant: the native multi-GPU product
+    partition (csrc/wm_dist.cpp) over an NCCL communicator of `world` ranks,
+    one per process (or thread) and GPU.  Rank 0 makes the 128-byte NCCL id
+    with ``DistContext.unique_id()`` and ships it to the others."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        rc = _lib.lib().wm_dist_unique_id(buf)
+        if rc:
+            raise _BY_CODE.get(rc, WinomemError)(_lib.lib().wm_dist_last_error().decode())
+        return buf.raw
+
+    def __init__(self, rank, world, uid: bytes, device=0, p=kDefaultModulus, real=False):
+        self.ctx = Context.get(device, p, real)
+        self.h = C.c_void_p()
+        rc = _lib.lib().wm_dist_create(self.ctx.h, rank, world, uid, C.byref(self.h))
+        if rc:
+            raise _BY_CODE.get(rc, WinomemError)(_lib.lib().wm_dist_last_error().decode())
+        self.rank, self.world = rank, world
+
+    def run_variant(self, variant, A=None, B=None, C_=None, alpha=1, beta=0, cutoff=1, levels=0,
+                    window=2) -> dict:
+        empty = wm_dmat(None, 0, 0, 0)
+        dm = lambda M: M.view().dmat() if M is not None else empty  # noqa: E731
+        r = _lib.wm_dist_report()
+        self.ctx.enter()
+        rc = _lib.lib().wm_dist_run_variant(self.h, variant.encode(), dm(A), dm(B), dm(C_), alpha,
+                                            beta, cutoff, levels, window, C.byref(r))
+        self.ctx.leave()
+        if rc:
+            raise _BY_CODE.get(rc, WinomemError)(_lib.lib().wm_dist_last_error().decode())
+        return dict(levels=r.levels, products=r.products, peak_extra_bytes=r.peak_extra_bytes,
+                    bytes_sent=r.bytes_sent, bytes_received=r.bytes_received)
+
+    def close(self):
+        if self.h:
+            _lib.lib().wm_dist_destroy(self.h)
+            self.h = None

@@ -69,3 +69,14 @@ def test_cpp_dropin_header_compiles():
         assert r.returncode == 0, r.stderr
         r = subprocess.run([exe, "--plan-only"], capture_output=True, text=True, timeout=60)
         assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_product_library_has_no_probes():
+    """The measurement probes (wm_diag_*) live in libwinomem_b200_diag.so only."""
+    from paper_0707_2347_b200 import _lib
+    L = ctypes.CDLL(_lib.PRODUCT_LIB)
+    for name in ("wm_diag_trace", "wm_diag_plan_dag", "wm_diag_direct_check", "wm_diag_chain",
+                 "wm_diag_time_leaf", "wm_diag_frame_gemm"):
+        assert not hasattr(L, name), name
+    D = ctypes.CDLL(_lib.DIAG_LIB)
+    assert hasattr(D, "wm_diag_direct_check") and hasattr(D, "wm_run_variant")

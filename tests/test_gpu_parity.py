@@ -516,3 +516,37 @@ def test_reference_acceptance_gate_on_b200():
     for crit in ("1", "2", "3", "4", "7"):
         line = next((l for l in out.splitlines() if f"criterion {crit} " in l), None)
         assert line is not None and line.startswith("[PASS]"), (crit, out)
+
+
+def test_native_dist_single_rank(W, O):
+    """The C-ABI multi-GPU partition (wm_dist_*, csrc/wm_dist.cpp) on a
+    one-rank NCCL communicator: the full protocol (shape / operand broadcasts,
+    per-rank operand formation, local in-place products, folds into C after
+    beta*C) at 7, 49 and 343 products, bit-exact vs the oracle; float64 within
+    the stated tolerance."""
+    uid = W.DistContext.unique_id()
+    D = W.DistContext(0, 1, uid)
+    try:
+        for levels in (1, 2, 3):
+            n = 512
+            A, B, C = _problem(W, n, n, n, 40 + levels, True)
+            a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+            rep = D.run_variant("std2", A, B, C, alpha=3, beta=5, cutoff=32, levels=levels)
+            assert rep["levels"] == levels and rep["products"] == 7 ** levels
+            assert (C.to_u32() == O.classical_modp(a0, b0, c0, 3, 5)).all(), levels
+            assert (A.to_u32() == a0).all() and (B.to_u32() == b0).all()  # read-only on the root
+            assert rep["peak_extra_bytes"] > 0
+    finally:
+        D.close()
+    Dr = W.DistContext(0, 1, W.DistContext.unique_id(), real=True)
+    try:
+        n = 1024
+        A, B, C = W.Matrix(n, n, real=True), W.Matrix(n, n, real=True), W.Matrix(n, n, real=True)
+        A.fill_random(5)
+        B.fill_random(6)
+        Dr.run_variant("std2", A, B, C, cutoff=64, levels=2)
+        ref = O.classical_f64(O.real_fill(n, n, 5), O.real_fill(n, n, 6))
+        err = np.linalg.norm(C.t.cpu().numpy() - ref) / np.linalg.norm(ref)
+        assert err <= 1e-12 * 2 ** 4, err
+    finally:
+        Dr.close()
