@@ -114,6 +114,7 @@ int wm_ctx_set_stream(wm_ctx* ctx, void* stream);
  *   "dead_hosts" [1]    frame planes in dead blocks (plan liveness)
  *   "cin_direct" [1]    accumulating frames: all planes outside C, C_in read by the combine
  *   "wide_plain" [1]    plain frames' GEMM at BN = 64 (c >= 256)
+ *   "micro" [1]         plans of tiny operations as one launch (shared-memory working set)
  *   "dag" [3]           issue lanes (concurrent streams); "epoch" [512] launches per join
  *   "stream_io" [1]     host u32 boundary streamed through the graph (pinned buffers)
  *   "leaf_kernel" [2]   0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto
