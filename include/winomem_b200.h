@@ -115,6 +115,8 @@ int wm_ctx_set_stream(wm_ctx* ctx, void* stream);
  *   "cin_direct" [1]    accumulating frames: all planes outside C, C_in read by the combine
  *   "wide_plain" [1]    plain frames' GEMM at BN = 64 (c >= 256)
  *   "micro" [1]         plans of tiny operations as one launch (shared-memory working set)
+ *   "arena_words"       (read-only) words of the context's temporary arena = the largest
+ *                       schedule peak run so far (one arena shared by every plan)
  *   "dag" [3]           issue lanes (concurrent streams); "epoch" [512] launches per join
  *   "stream_io" [1]     host u32 boundary streamed through the graph (pinned buffers)
  *   "leaf_kernel" [2]   0 = DMMA float64, 1 = tcgen05 int8 limbs, 2 = auto

@@ -77,10 +77,10 @@ cudaError_t launch_leaf_dmma(const MulParams& P, bool real, cudaStream_t s);
 cudaError_t launch_lincomb(const LincombParams& L, bool real, cudaStream_t s);
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,
                               std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
-                              cudaStream_t s);
+                              cudaStream_t s, unsigned long long* tl = nullptr);
 cudaError_t launch_f64_to_u32(std::uint32_t* dst, std::uint64_t ldd, const double* src,
                               std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
-                              std::uint32_t p, cudaStream_t s);
+                              std::uint32_t p, cudaStream_t s, unsigned long long* tl = nullptr);
 cudaError_t launch_fill_splitmix(double* dst, std::uint64_t ld, std::uint64_t rows,
                                  std::uint64_t cols, std::uint64_t seed, std::uint32_t p,
                                  bool real, cudaStream_t s);

@@ -108,19 +108,23 @@ __global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams
 
 __global__ void k_u32_to_f64(double* __restrict__ dst, std::uint64_t ldd,
                              const std::uint32_t* __restrict__ src, std::uint64_t lds,
-                             std::uint64_t rows, std::uint64_t cols) {
+                             std::uint64_t rows, std::uint64_t cols, unsigned long long* tl) {
+    WM_TL_BEGIN(tl);
     const std::uint64_t total = rows * cols;
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
          i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
         const std::uint64_t r = i / cols, c = i - r * cols;
         dst[r * ldd + c] = static_cast<double>(src[r * lds + c]);
     }
+    WM_TL_END(tl);
 }
 
 // canonicalise (values are exact integers; reduce any representative into [0, p))
 __global__ void k_f64_to_u32(std::uint32_t* __restrict__ dst, std::uint64_t ldd,
                              const double* __restrict__ src, std::uint64_t lds,
-                             std::uint64_t rows, std::uint64_t cols, double p) {
+                             std::uint64_t rows, std::uint64_t cols, double p,
+                             unsigned long long* tl) {
+    WM_TL_BEGIN(tl);
     const std::uint64_t total = rows * cols;
     for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
          i < total; i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
@@ -131,6 +135,7 @@ __global__ void k_f64_to_u32(std::uint32_t* __restrict__ dst, std::uint64_t ldd,
         if (v < 0) v += p;
         dst[r * ldd + c] = static_cast<std::uint32_t>(v);
     }
+    WM_TL_END(tl);
 }
 
 __device__ __forceinline__ std::uint64_t sm64_mix(std::uint64_t z) {
@@ -264,16 +269,16 @@ cudaError_t launch_lincomb(const LincombParams& L, bool real, cudaStream_t s) {
 
 cudaError_t launch_u32_to_f64(double* dst, std::uint64_t ldd, const std::uint32_t* src,
                               std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
-                              cudaStream_t s) {
-    k_u32_to_f64<<<grid_for(rows * cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols);
+                              cudaStream_t s, unsigned long long* tl) {
+    k_u32_to_f64<<<grid_for(rows * cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols, tl);
     return cudaGetLastError();
 }
 
 cudaError_t launch_f64_to_u32(std::uint32_t* dst, std::uint64_t ldd, const double* src,
                               std::uint64_t lds, std::uint64_t rows, std::uint64_t cols,
-                              std::uint32_t p, cudaStream_t s) {
+                              std::uint32_t p, cudaStream_t s, unsigned long long* tl) {
     k_f64_to_u32<<<grid_for(rows * cols), 256, 0, s>>>(dst, ldd, src, lds, rows, cols,
-                                                        static_cast<double>(p));
+                                                        static_cast<double>(p), tl);
     return cudaGetLastError();
 }
 

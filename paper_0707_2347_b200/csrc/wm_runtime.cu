@@ -161,7 +161,6 @@ struct CachedPlan {
     Plan plan;
     std::vector<Step> steps;
     std::shared_ptr<DagPlan> dag;  // concurrent issue plan (lanes option)
-    double* arena = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     unsigned long long* tl = nullptr;  // measurement timeline (trace option)
@@ -174,7 +173,6 @@ struct CachedPlan {
         if (micro) cudaFree(micro);
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
-        if (arena) cudaFree(arena);
     }
 };
 
@@ -224,6 +222,11 @@ struct wm_ctx {
     Lanes lanes;
     // plan cache (small LRU)
     std::list<std::pair<std::string, std::unique_ptr<CachedPlan>>> cache;
+    // one arena of schedule temporaries for every plan of this context (plans
+    // run one after the other on its stream), sized to the largest high-water
+    // mark: the process holds exactly the schedule's peak extra memory
+    double* arena = nullptr;
+    std::uint64_t arena_words = 0;
     // boundary staging
     std::uint32_t* stage = nullptr;
     std::size_t stage_words = 0;
@@ -232,6 +235,7 @@ struct wm_ctx {
 
     ~wm_ctx() {
         cache.clear();
+        if (arena) cudaFree(arena);
         if (stage) cudaFree(stage);
         for (auto* b : hbuf)
             if (b) cudaFree(b);
@@ -1044,11 +1048,12 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
             WM_CUDA(cudaMemcpy2DAsync(s.sptr, s.sld * 4, s.hptr, s.hld * 4, s.io_cols * 4, s.io_rows,
                                       cudaMemcpyHostToDevice, st));
             g_pdl = false;
-            WM_CUDA(launch_u32_to_f64(s.dptr, s.dld, s.sptr, s.sld, s.io_rows, s.io_cols, st));
+            WM_CUDA(launch_u32_to_f64(s.dptr, s.dld, s.sptr, s.sld, s.io_rows, s.io_cols, st, s.tl));
             break;
         case Step::DOWNLOAD:
             g_pdl = false;
-            WM_CUDA(launch_f64_to_u32(s.sptr, s.sld, s.dptr, s.dld, s.io_rows, s.io_cols, s.io_p, st));
+            WM_CUDA(launch_f64_to_u32(s.sptr, s.sld, s.dptr, s.dld, s.io_rows, s.io_cols, s.io_p, st,
+                                      s.tl));
             WM_CUDA(cudaMemcpy2DAsync(s.hptr, s.hld * 4, s.sptr, s.sld * 4, s.io_cols * 4, s.io_rows,
                                       cudaMemcpyDeviceToHost, st));
             break;
@@ -1291,10 +1296,10 @@ void add_io_steps(std::vector<Step>& steps, const HostIO& io, const wm_dmat M[3]
     for (int w = 0; w < 3; ++w) {
         if (!io.up[w] && !io.down[w]) continue;
         const std::uint64_t r = M[w].rows, c = M[w].cols;
-        const bool quads = r % 2 == 0 && c % 2 == 0;
-        for (int q = 0; q < (quads ? 4 : 1); ++q) {
-            const std::uint64_t br = quads ? r / 2 : r, bc = quads ? c / 2 : c;
-            const std::uint64_t r0 = quads ? (q / 2) * br : 0, c0 = quads ? (q % 2) * bc : 0;
+        const int parts = r % 2 == 0 && c % 2 == 0 ? 2 : 1;  // quadrants
+        for (int q = 0; q < parts * parts; ++q) {
+            const std::uint64_t br = r / parts, bc = c / parts;
+            const std::uint64_t r0 = (q / parts) * br, c0 = (q % parts) * bc;
             Step st{};
             st.hptr = io.h[w] + r0 * c + c0;
             st.sptr = io.stage[w] + r0 * c + c0;
@@ -1346,6 +1351,20 @@ void add_io_steps(std::vector<Step>& steps, const HostIO& io, const wm_dmat M[3]
     for (Step& st : steps) out.push_back(std::move(st));
     for (Step& st : downs) out.push_back(std::move(st));
     steps.swap(out);
+}
+
+// Grow the context's arena to `words` (cached plans embed its address: they
+// are dropped, after the stream has drained, when it moves).
+void ensure_arena(wm_ctx* ctx, std::uint64_t words) {
+    if (words <= ctx->arena_words) return;
+    WM_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->cache.clear();
+    ctx->traced = nullptr;
+    if (ctx->arena) WM_CUDA(cudaFree(ctx->arena));
+    ctx->arena = nullptr;
+    ctx->arena_words = 0;
+    WM_CUDA(cudaMalloc(&ctx->arena, words * sizeof(double)));
+    ctx->arena_words = words;
 }
 
 // A plan whose every operation is tiny (the unit-size recursions of the
@@ -1453,9 +1472,8 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
         auto np = std::make_unique<CachedPlan>();
         np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld, alpha,
                                 beta, cutoff, opt);
-        if (np->plan.arena_words)
-            WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
-        double* base[4] = {A.ptr, B.ptr, C.ptr, np->arena};
+        ensure_arena(ctx, np->plan.arena_words);
+        double* base[4] = {A.ptr, B.ptr, C.ptr, ctx->arena};
         if (!io && micro_plan(*ctx, np->plan, base, *np, A, B, C)) {
             // tiny plan: nothing to lower
         } else try {
@@ -1465,15 +1483,10 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
             // every frame unfused (nothing has been issued yet)
             if (e.code != E_INVALID || !opt.fuse_frames) throw;
             opt.fuse_frames = false;
-            const std::uint64_t had = np->plan.arena_words;
             np->plan = plan_variant(variant, ctx->f, A.rows, A.cols, B.cols, A.ld, B.ld, C.ld,
                                     alpha, beta, cutoff, opt);
-            if (np->plan.arena_words > had) {
-                WM_CUDA(cudaFree(np->arena));
-                np->arena = nullptr;
-                WM_CUDA(cudaMalloc(&np->arena, np->plan.arena_words * sizeof(double)));
-                base[3] = np->arena;
-            }
+            ensure_arena(ctx, np->plan.arena_words);
+            base[3] = ctx->arena;
             np->steps = lower(np->plan, base, *ctx);
         }
         if (io) {
@@ -1781,6 +1794,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "fold") *value = ctx->fold;
         else if (k == "stream_io") *value = ctx->stream_io;
         else if (k == "micro") *value = ctx->micro;
+        else if (k == "arena_words") *value = static_cast<int64_t>(ctx->arena_words);  // read-only
         else if (k == "dead_hosts") *value = ctx->dead_hosts;
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;

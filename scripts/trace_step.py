@@ -17,7 +17,7 @@ import bench  # noqa: E402
 import paper_0707_2347_b200 as W  # noqa: E402
 from paper_0707_2347_b200._lib import lib  # noqa: E402
 
-KINDS = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "COOP", "UPLOAD", "DOWNLOAD"]
+KINDS = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "UPLOAD", "DOWNLOAD"]
 
 
 def main():
@@ -58,6 +58,10 @@ def main():
     assert rc == 0, L.wm_last_error()
     n_ = nn.value
     start, end, kind, lane = start[:n_], end[:n_], kind[:n_], lane[:n_]
+    dump = os.environ.get("WM_TRACE_DUMP")
+    if dump:  # the raw timeline, for offline analysis
+        json.dump({"start": start.tolist(), "end": end.tolist(), "kind": kind.tolist(),
+                   "lane": lane.tolist()}, open(dump, "w"))
     waits = waits[:4 * n_].reshape(n_, 4)
     prev_on_lane = np.full(n_, -1)
     last = {}

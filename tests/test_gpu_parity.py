@@ -550,3 +550,29 @@ def test_native_dist_single_rank(W, O):
         assert err <= 1e-12 * 2 ** 4, err
     finally:
         Dr.close()
+
+
+def test_context_arena_is_the_schedule_peak(W):
+    """One arena per context, shared by its plans: the HBM the process holds for
+    temporaries equals the largest schedule peak run so far (words x 8 B)."""
+    ctx = W.Context(0, 65521)  # a fresh context
+    try:
+        def run(v, n, c, acc):
+            A, B, C = _problem(W, n, n, n, 3, acc)
+            import ctypes
+            from paper_0707_2347_b200 import _lib
+            rep = _lib.wm_report()
+            rc = _lib.lib().wm_run_variant(ctx.h, v.encode(), A.view().dmat(), B.view().dmat(),
+                                            C.view().dmat(), 1, 1 if acc else 0, c, ctypes.byref(rep))
+            assert rc == 0, _lib.last_error()
+            ctx.sync()
+            return rep.peak_extra_words
+        p1 = run("std2", 1024, 128, False)
+        assert ctx.get_option("arena_words") == p1 == 688128
+        p2 = run("acc2", 512, 64, True)
+        assert p2 < p1 and ctx.get_option("arena_words") == p1
+        p3 = run("acc2", 2048, 128, True)
+        assert p3 > p1 and ctx.get_option("arena_words") == p3
+        run("std2", 1024, 128, False)  # plans made before the arena moved are rebuilt
+    finally:
+        ctx.close()
