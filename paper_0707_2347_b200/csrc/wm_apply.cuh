@@ -46,23 +46,6 @@ __device__ __forceinline__ double apply(double a, double b, std::uint32_t mode, 
 }
 
 namespace fused {
-// Lazy residue arithmetic of a fused run: +/- chains skip the conditional
-// correction (values stay exact integers, |v| < 2^16 * 2^kMaxIns); scaled terms
-// are reduced (their operands may be unreduced: |sa a + sb b| < 2^50, exact).
-template <bool REAL>
-__device__ __forceinline__ double lop(std::uint32_t mode, double a, double b, double sa,
-                                      double sb, double p, double pinv) {
-    if (REAL) return apply<true>(a, b, mode, sa, sb, p, pinv);
-    switch (mode) {
-        case M_ADD: return a + b;
-        case M_SUB: return a - b;
-        case M_RSUB: return b - a;
-        case M_NEGADD: return -(a + b);
-        case M_COPY: return a;
-        case M_NEG: return -a;
-        default: return apply<false>(a, b, mode, sa, sb, p, pinv);  // |operands| < 2^24: exact
-    }
-}
 // canonical representative in [0, p) of an exact integer value
 template <bool REAL>
 __device__ __forceinline__ double canon(double v, double p, double pinv) {

@@ -89,9 +89,9 @@ namespace {
 // One fused run of a schedule's block additions: every thread owns one 16-B
 // position of the (identically shaped, pairwise disjoint) slot views and
 // executes the run's dataflow on registers -- each slot read once, written once.
-template <bool REAL>
-__global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams G,
-                                                unsigned long long* tl) {
+// One kernel per run (GID): each launch carries only its own body.
+template <bool REAL, int GID>
+__global__ void __launch_bounds__(256) k_group(const fused::GroupParams G, unsigned long long* tl) {
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     WM_PDL_EARLY_M();
     WM_TL_BEGIN(tl);
@@ -100,11 +100,20 @@ __global__ void __launch_bounds__(256) k_group(int gid, const fused::GroupParams
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
     if (idx < total) {
         const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
-        fused::group_dispatch<REAL>(gid, G, r, c);
+        fused::GroupBody<REAL, GID>::run(G, r, c);
     }
     WM_TL_END(tl);
     WM_PDL_LATE_M();
 }
+
+using GroupKernel = void (*)(const fused::GroupParams, unsigned long long*);
+#define WM_GK_MODP(i) k_group<false, i>,
+#define WM_GK_REAL(i) k_group<true, i>,
+const GroupKernel kGroupModp[] = {WM_FUSED_GROUP_IDS(WM_GK_MODP)};
+const GroupKernel kGroupReal[] = {WM_FUSED_GROUP_IDS(WM_GK_REAL)};
+#undef WM_GK_MODP
+#undef WM_GK_REAL
+static_assert(sizeof(kGroupModp) / sizeof(kGroupModp[0]) == fused::kNumGroups, "one kernel per run");
 
 __global__ void k_u32_to_f64(double* __restrict__ dst, std::uint64_t ldd,
                              const std::uint32_t* __restrict__ src, std::uint64_t lds,
@@ -248,8 +257,8 @@ cudaError_t launch_group(int gid, const fused::GroupParams& G, bool real, cudaSt
     attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (real) return cudaLaunchKernelEx(&cfg, k_group<true>, gid, G, tl);
-    return cudaLaunchKernelEx(&cfg, k_group<false>, gid, G, tl);
+    if (gid < 0 || gid >= fused::kNumGroups) return cudaErrorInvalidValue;
+    return cudaLaunchKernelEx(&cfg, real ? kGroupReal[gid] : kGroupModp[gid], G, tl);
 }
 
 cudaError_t launch_lincomb(const LincombParams& L, bool real, cudaStream_t s) {

@@ -380,11 +380,20 @@ bool try_group(const Plan& plan, std::size_t i, int g, double* const base[4], St
     }
     for (int j = 0; j < G.nins; ++j) {
         const Op& op = plan.ops[i + j];
-        st.grp.mode[j] = op.kind == OP_ADDSUB
-                             ? modp_add_mode(f, op.sa, op.sb)
-                             : (f.is_one(op.sa) ? M_COPY : f.is_minus_one(op.sa) ? M_NEG : M_SCALE);
-        st.grp.sa[j] = f.real ? op.sa.d : static_cast<double>(op.sa.r);
-        st.grp.sb[j] = f.real ? op.sb.d : static_cast<double>(op.sb.r);
+        // s_dst = ca * s_a + cb * s_b: unit scalars as +-1 (lazy), others as residues
+        // whose result is reduced at once
+        auto coef = [&](Scalar v, bool* general) {
+            if (f.real) return v.d;
+            if (f.is_zero(v)) return 0.0;
+            if (f.is_one(v)) return 1.0;
+            if (f.is_minus_one(v)) return -1.0;
+            *general = true;
+            return static_cast<double>(v.r);
+        };
+        bool general = false;
+        st.grp.ca[j] = coef(op.sa, &general);
+        st.grp.cb[j] = op.kind == OP_ADDSUB ? coef(op.sb, &general) : 0.0;
+        if (general) st.grp.gen |= 1u << j;
     }
     st.grp.rows = static_cast<std::uint32_t>(first.d.rows);
     st.grp.cols = static_cast<std::uint32_t>(first.d.cols);

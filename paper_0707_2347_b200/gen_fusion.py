@@ -175,8 +175,11 @@ def main():
     w("struct GroupParams {")
     w("    double* v[kMaxSlots];")
     w("    std::uint64_t ld[kMaxSlots];")
-    w("    std::uint32_t mode[kMaxIns];")
-    w("    double sa[kMaxIns], sb[kMaxIns];")
+    w("    // instruction j: s_dst = ca[j] * s_a + cb[j] * s_b (cb = 0 for a one-term copy);")
+    w("    // +-1 / 0 coefficients stay unreduced (lazy), bit j of `gen` marks a general")
+    w("    // scalar whose result is reduced at once (MODP)")
+    w("    double ca[kMaxIns], cb[kMaxIns];")
+    w("    std::uint32_t gen;")
     w("    std::uint32_t rows, cols;  // cols even, all views 16-B aligned")
     w("    double p, pinv;")
     w("};")
@@ -184,10 +187,12 @@ def main():
     w("// lazy modular reduction (wm_apply.cuh): a run's intermediate values stay")
     w("// unreduced (exact integers in float64); every stored slot is canonicalised once")
     w("template <bool REAL>")
-    w("__device__ __forceinline__ double lop(std::uint32_t mode, double a, double b, double sa,")
-    w("                                      double sb, double p, double pinv);")
-    w("template <bool REAL>")
     w("__device__ __forceinline__ double canon(double v, double p, double pinv);")
+    w("template <bool REAL>")
+    w("__device__ __forceinline__ double lin(const GroupParams& G, int j, double a, double b) {")
+    w("    const double v = fma(G.ca[j], a, G.cb[j] * b);  // branch-free: no per-mode switch")
+    w("    return (!REAL && ((G.gen >> j) & 1u)) ? canon<REAL>(v, G.p, G.pinv) : v;")
+    w("}")
     w("")
     w("// LDG: read-only path for slots nothing in the kernel writes")
     w("template <bool LDG>")
@@ -211,24 +216,26 @@ def main():
         for j, (_, kind, dst, ops) in enumerate(g["run"]):
             d, a = idx[dst], idx[ops[0]]
             b = idx[ops[1]] if kind == "add" else a
-            w(f"    s{d} = make_double2(lop<REAL>(G.mode[{j}], s{a}.x, s{b}.x, G.sa[{j}], "
-              f"G.sb[{j}], G.p, G.pinv), lop<REAL>(G.mode[{j}], s{a}.y, s{b}.y, G.sa[{j}], "
-              f"G.sb[{j}], G.p, G.pinv));")
+            w(f"    s{d} = make_double2(lin<REAL>(G, {j}, s{a}.x, s{b}.x), "
+              f"lin<REAL>(G, {j}, s{a}.y, s{b}.y));")
         for s in g["stores"]:
             i = idx[s]
             w(f"    *reinterpret_cast<double2*>(G.v[{i}] + r * G.ld[{i}] + c) = "
               f"make_double2(canon<REAL>(s{i}.x, G.p, G.pinv), canon<REAL>(s{i}.y, G.p, G.pinv));")
         w("}")
         w("")
-    w("template <bool REAL, bool LDG = true>")
-    w("__device__ __forceinline__ void group_dispatch(int gid, const GroupParams& G,"
-      " std::uint64_t r, std::uint64_t c) {")
-    w("    switch (gid) {")
+    w("// one kernel per run (wm_kernels.cu instantiates k_group<REAL, G> for every G):")
+    w("// each launch runs only its own compact body -- no dispatch switch, no jump table")
+    w("template <bool REAL, int G>")
+    w("struct GroupBody;")
     for gi in range(len(groups)):
-        w(f"        case {gi}: group_body_{gi}<REAL, LDG>(G, r, c); break;")
-    w("        default: break;")
-    w("    }")
-    w("}")
+        w(f"template <bool REAL> struct GroupBody<REAL, {gi}> {{")
+        w("    static __device__ __forceinline__ void run(const GroupParams& P, std::uint64_t r,"
+          " std::uint64_t c) {")
+        w(f"        group_body_{gi}<REAL, true>(P, r, c);")
+        w("    }")
+        w("};")
+    w("#define WM_FUSED_GROUP_IDS(X) " + " ".join(f"X({gi})" for gi in range(len(groups))))
     w("}  // namespace fused")
     w("}  // namespace wm")
     text = "\n".join(L) + "\n"
