@@ -29,6 +29,7 @@ struct AddItem {
     std::uint32_t mode;
     std::uint32_t sa, sb;  // residues (MODP)
     double sad, sbd;       // values (REAL64)
+    double ca, cb;         // d = ca*a + cb*b (then reduced, MODP): the branch-free form k_addsub runs
     std::uint32_t blk0;    // first block of this item within the launch
     std::uint32_t vec;     // 2: 16-byte vector path, 1: scalar path
 };

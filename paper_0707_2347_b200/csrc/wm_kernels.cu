@@ -20,6 +20,18 @@ namespace wm {
 bool g_pdl = true;
 namespace {
 
+// d = ca*a + cb*b over canonical operands, reduced once (MODP: residue
+// scalars, |v| < 2^33, exact): one FMA path for every addition mode
+template <bool REAL>
+__device__ __forceinline__ double lin_item(double a, double b, double ca, double cb, double p,
+                                           double pinv) {
+    const double v = fma(ca, a, cb * b);
+    if (REAL) return v;
+    double r = fma(-floor(v * pinv), p, v);
+    r = r < 0.0 ? r + p : r;
+    return r >= p ? r - p : r;
+}
+
 template <bool REAL, int ILP>
 __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
     // programmatic dependent launch: wait for the producer grid, then let the
@@ -32,8 +44,6 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
     while (i + 1 < B.n && blockIdx.x >= B.it[i + 1].blk0) ++i;
     const AddItem& t = B.it[i];
     const std::uint32_t mode = t.mode;
-    const double sa = REAL ? t.sad : static_cast<double>(t.sa);
-    const double sb = REAL ? t.sbd : static_cast<double>(t.sb);
     const double p = B.pd, pinv = B.pinv;
     const bool two = mode <= M_GEN;
     const std::uint64_t blk = blockIdx.x - t.blk0;
@@ -59,8 +69,8 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
         for (int u = 0; u < ILP; ++u) {
             if (!ok[u]) continue;
             double2 o;
-            o.x = apply<REAL>(av[u].x, two ? bv[u].x : 0.0, mode, sa, sb, p, pinv);
-            o.y = apply<REAL>(av[u].y, two ? bv[u].y : 0.0, mode, sa, sb, p, pinv);
+            o.x = lin_item<REAL>(av[u].x, two ? bv[u].x : 0.0, t.ca, t.cb, p, pinv);
+            o.y = lin_item<REAL>(av[u].y, two ? bv[u].y : 0.0, t.ca, t.cb, p, pinv);
             *reinterpret_cast<double2*>(t.d + r[u] * t.ldd + c[u]) = o;
         }
     } else {
@@ -73,7 +83,7 @@ __global__ void __launch_bounds__(kAddThreads) k_addsub(const AddBatch B) {
             const std::uint64_t rr = idx / t.cols, cc = idx - rr * t.cols;
             const double a = t.a[rr * t.lda + cc];
             const double b = two ? t.b[rr * t.ldb + cc] : 0.0;
-            t.d[rr * t.ldd + cc] = apply<REAL>(a, b, mode, sa, sb, p, pinv);
+            t.d[rr * t.ldd + cc] = lin_item<REAL>(a, b, t.ca, t.cb, p, pinv);
         }
     }
     WM_TL_END(B.tl);

@@ -282,6 +282,8 @@ AddItem make_item(const Op& op, const Field& f, double* const base[4]) {
         t.mode = f.is_one(op.sa) ? M_COPY : f.is_minus_one(op.sa) ? M_NEG : M_SCALE;
     }
     t.vec = vec ? 2 : 1;
+    t.ca = f.real ? op.sa.d : static_cast<double>(op.sa.r);
+    t.cb = op.kind != OP_ADDSUB ? 0.0 : f.real ? op.sb.d : static_cast<double>(op.sb.r);
     return t;
 }
 
