@@ -1,4 +1,3 @@
-for cfg in C2 C1 C3 C4 C5; do timeout 900 python bench.py --config $cfg --steps 10 --warmup 3 > gpurun_out/bench_$cfg.json 2>gpurun_out/bench_$cfg.err; echo $cfg rc=$?; done
-timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_C2.json 2>gpurun_out/bench_ref_C2.err; echo ref rc=$?
+for o in dag=2 dag=3 dag=4 dag=5 dag=6 epoch=1024 wide_plain=0; do WM_OPTS=$o timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/sweep_$o.json 2>&1; python -c "import json; d=json.load(open('gpurun_out/sweep_$o.json')); print('$o', round(d['ms_per_step'],3))"; done
 python scripts/one_step.py C2 > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_c2.csv python scripts/one_step.py C2 > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_group" -s 60 -c 4 -o gpurun_out/prof_group2_c2 python scripts/one_step.py C2 > gpurun_out/ncu_full4.log 2>&1; echo ncu rc=$?
