@@ -198,6 +198,10 @@ int wm_expected_costs(const char* variant, uint64_t m, uint64_t k, uint64_t n, i
                       wm_report* report);
 /* Per-schedule frame counts of the last plan on this thread: "name:count,..." */
 int wm_plan_schedule_calls(char* out, int len);
+/* CostMeter::alloc_log of the last plan on this thread (meter.hpp:15-19, 40-45):
+ * "words:depth:slot;..." per metered temporary, in acquisition order; returns
+ * the full length (call with out = NULL to size the buffer) */
+int wm_plan_alloc_log(char* out, int len);
 
 /* Schedule DSL (schedule.hpp:261-684, executor.hpp:304-342).
  * wm_run_parsed_schedule: run_parsed_schedule -- the schedule in `text` runs at

@@ -439,6 +439,18 @@ inline CostReport to_report(const std::string& v, std::size_t m, std::size_t k, 
         meter->classical_calls += r.classical_calls;
         meter->peak_extra_bytes = r.peak_extra_bytes;
         meter->launches = r.n_launches;
+        const int need = wm_plan_alloc_log(nullptr, 0);
+        std::string log(static_cast<std::size_t>(need) + 1, '\0');
+        wm_plan_alloc_log(&log[0], need + 1);
+        log.resize(static_cast<std::size_t>(need));
+        std::istringstream ls(log);
+        std::string ev;
+        while (std::getline(ls, ev, ';')) {
+            const auto c1 = ev.find(':'), c2 = ev.find(':', c1 + 1);
+            if (c1 == std::string::npos || c2 == std::string::npos) continue;
+            meter->alloc_log.push_back({std::stoull(ev.substr(0, c1)),
+                                        std::stoi(ev.substr(c1 + 1, c2 - c1 - 1)), ev.substr(c2 + 1)});
+        }
         char buf[4096];
         wm_plan_schedule_calls(buf, sizeof(buf));
         std::string s(buf), item;

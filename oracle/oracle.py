@@ -189,6 +189,19 @@ def ref_primitive_on_windows(op, buf, wins, s0, s1=0, p=DEFAULT_P):
     return rc, out
 
 
+def ref_alloc_log(variant, m, k, n, alpha=1, beta=0, cutoff=1):
+    """The reference CostMeter's alloc_log of run_variant, as "words:depth:slot;..."."""
+    L = ref()
+    f = L.ref_alloc_log
+    f.argtypes = [C.c_char_p, u64, u64, u64, u32, u32, C.c_int, C.c_char_p, C.c_int]
+    f.restype = C.c_int
+    buf = C.create_string_buffer(1 << 22)
+    rc = f(variant.encode(), m, k, n, alpha, beta, cutoff, buf, 1 << 22)
+    if rc < 0:
+        raise RefError(-rc, "reference raised")
+    return buf.value.decode()
+
+
 def ref_expected_costs(variant, m, k, n, cutoff):
     rep = np.zeros(6, dtype=np.uint64)
     err = C.create_string_buffer(512)

@@ -199,6 +199,32 @@ int ref_primitive_on_windows(int op, std::uint64_t rows, std::uint64_t cols, std
     }
 }
 
+// run_variant with a CostMeter: its alloc_log (meter.hpp:15-19, 40-45) as
+// "words:depth:slot;..." (returns the full length, or -code on an exception)
+int ref_alloc_log(const char* variant, std::uint64_t m, std::uint64_t k, std::uint64_t n,
+                  std::uint32_t alpha, std::uint32_t beta, int cutoff, char* out, int len) {
+    try {
+        Modulus mod(65521);
+        Matrix A(m, k, mod), B(k, n, mod), C(m, n, mod);
+        A.fill_random(1);
+        B.fill_random(2);
+        C.fill_random(3);
+        CostMeter meter;
+        MultiplyOptions opt;
+        opt.alpha = alpha;
+        opt.beta = beta;
+        opt.cutoff = cutoff;
+        run_variant(variant, A, B, C, opt, &meter);
+        std::string text;
+        for (const auto& e : meter.alloc_log)
+            text += std::to_string(e.words) + ":" + std::to_string(e.depth) + ":" + e.slot + ";";
+        put_err(out, len, text.c_str());
+        return static_cast<int>(text.size());
+    } catch (const std::exception& e) {
+        return -code_of(e);
+    }
+}
+
 void ref_fill_random(std::uint32_t* out, std::uint64_t count, std::uint64_t seed,
                      std::uint32_t p) {
     SplitMix64 g(seed);

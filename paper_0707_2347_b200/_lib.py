@@ -26,6 +26,7 @@ EXPORTS = [
     "wm_ctx_set_option", "wm_ctx_get_option", "wm_block_addsub", "wm_block_scale_copy",
     "wm_classical_mul", "wm_run_variant", "wm_ipmm", "wm_run_variant_real",
     "wm_run_variant_host_u32", "wm_plan_report", "wm_expected_costs", "wm_plan_schedule_calls",
+    "wm_plan_alloc_log",
     "wm_upload_u32", "wm_download_u32", "wm_fnv1a64_u32", "wm_fill_random",
     "wm_run_parsed_schedule", "wm_parse_schedule", "wm_render_schedule",
     "wm_run_parsed_schedule_host_u32", "wm_matrix_file_info", "wm_matrix_read_host",
@@ -91,6 +92,7 @@ def lib():
                                  P(wm_report)]
     L.wm_expected_costs.argtypes = [C.c_char_p, u64, u64, u64, i32, P(wm_report)]
     L.wm_plan_schedule_calls.argtypes = [C.c_char_p, i32]
+    L.wm_plan_alloc_log.argtypes = [C.c_char_p, i32]
     L.wm_upload_u32.argtypes = [ctx_p, wm_dmat, C.c_void_p, u64]
     L.wm_download_u32.argtypes = [ctx_p, C.c_void_p, u64, wm_dmat]
     L.wm_fnv1a64_u32.argtypes = [C.c_void_p, u64]

@@ -54,7 +54,7 @@ void ArenaWorkspace::push_frame() {
     words_.emplace_back();
 }
 
-View ArenaWorkspace::acquire(std::uint64_t rows, std::uint64_t cols, int, const char*) {
+View ArenaWorkspace::acquire(std::uint64_t rows, std::uint64_t cols, int depth, const char* slot) {
     if (marks_.empty()) fail(E_WORKSPACE, "acquire outside a frame");
     // 256-byte aligned placement keeps every temporary 16-B vector / TMA aligned;
     // at the BASELINE sizes (temporaries >= 128 x 128) it adds no padding.
@@ -62,7 +62,7 @@ View ArenaWorkspace::acquire(std::uint64_t rows, std::uint64_t cols, int, const 
     used_ = off + rows * cols;
     high_ = std::max(high_, used_);
     words_.back().push_back(rows * cols);
-    if (meter_) meter_->on_alloc(rows * cols);
+    if (meter_) meter_->on_alloc(rows * cols, depth, slot);
     View v;
     v.region = R_T;
     v.origin = next_origin_++;
@@ -697,6 +697,8 @@ Plan plan_variant(const std::string& variant, Field f, std::uint64_t m, std::uin
         }
     }
     plan.arena_words = heap.high_water();
+    plan.alloc_log = std::make_shared<const std::vector<Meter::AllocEvent>>(
+        std::move(plan.meter.alloc_log));
     return plan;
 }
 

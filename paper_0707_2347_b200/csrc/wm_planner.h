@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -43,6 +44,8 @@ struct Plan {
     std::vector<Op> ops;
     Meter meter;
     std::uint64_t arena_words = 0;  // physical high-water of the temporary arena
+    // the meter's allocation trace, shared (not copied) with every report of this plan
+    std::shared_ptr<const std::vector<Meter::AllocEvent>> alloc_log;
 };
 
 struct Workspace {

@@ -47,6 +47,8 @@ namespace {
 
 thread_local std::string g_err;
 thread_local std::string g_sched_calls;
+// allocation trace of the last plan reported on this thread (shared with the plan)
+thread_local std::shared_ptr<const std::vector<Meter::AllocEvent>> g_alloc_log;
 
 int set_err(int code, const std::string& msg) {
     g_err = msg;
@@ -1269,6 +1271,7 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
         first = false;
     }
     g_sched_calls = os.str();
+    g_alloc_log = plan.alloc_log;
 }
 
 Scalar modp_scalar(const Field& f, std::uint32_t v) {
@@ -2105,6 +2108,18 @@ int wm_matrix_write_device(wm_ctx* ctx, const char* path, int binary, wm_dmat sr
         WM_CUDA(cudaStreamSynchronize(ctx->stream));
         write_matrix_file(path ? path : "", binary != 0, src.rows, src.cols, ctx->f.p, h.data());
     });
+}
+
+int wm_plan_alloc_log(char* out, int len) {
+    std::ostringstream al;
+    if (g_alloc_log)
+        for (const auto& e : *g_alloc_log) al << e.words << ':' << e.depth << ':' << e.slot << ';';
+    const std::string text = al.str();
+    if (out && len > 0) {
+        std::strncpy(out, text.c_str(), static_cast<std::size_t>(len) - 1);
+        out[len - 1] = 0;
+    }
+    return static_cast<int>(text.size());
 }
 
 int wm_plan_schedule_calls(char* out, int len) {

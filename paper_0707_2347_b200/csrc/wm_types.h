@@ -143,7 +143,15 @@ struct Meter {
     std::uint64_t add2_elems = 0;   // elements of two-term additions (3 words moved each)
     std::uint64_t copy_elems = 0;   // elements of copies / scalings (2 words each)
     std::uint64_t leaf_flops = 0;   // sum of 2*m*k*n over classical leaves
-    void on_alloc(std::uint64_t w) {
+    // CostMeter::alloc_log (meter.hpp:15-19, 40-45): every metered temporary
+    struct AllocEvent {
+        std::uint64_t words;
+        int depth;
+        const char* slot;  // static slot name
+    };
+    std::vector<AllocEvent> alloc_log;
+    void on_alloc(std::uint64_t w, int depth = 0, const char* slot = "") {
+        alloc_log.push_back({w, depth, slot});
         live += w;
         if (live > peak) peak = live;
         total += w;

@@ -180,6 +180,21 @@ class CostReport:
                 f"{self.adds},{self.peak_extra_words},{self.total_alloc_words}")
 
 
+def last_alloc_log():
+    """CostMeter::alloc_log (meter.hpp:15-19) of the last plan on this thread:
+    [(words, depth, slot), ...] in acquisition order."""
+    L = _lib.lib()
+    need = L.wm_plan_alloc_log(None, 0)
+    buf = C.create_string_buffer(need + 1)
+    L.wm_plan_alloc_log(buf, need + 1)
+    out = []
+    for ev in buf.value.decode().split(";"):
+        if ev:
+            w, d, slot = ev.split(":", 2)
+            out.append((int(w), int(d), slot))
+    return out
+
+
 def _report(variant, m, k, n, cutoff, r: wm_report) -> CostReport:
     buf = C.create_string_buffer(4096)
     _lib.lib().wm_plan_schedule_calls(buf, 4096)

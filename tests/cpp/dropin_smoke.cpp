@@ -188,6 +188,9 @@ int main(int argc, char** argv) {
             std::printf("%s mismatch\n", v);
             return 10;
         }
+        std::uint64_t logged = 0;  // alloc_log (meter.hpp:15-19) sums to the total
+        for (const auto& e : meter.alloc_log) logged += e.words;
+        if (logged != meter.total_alloc_words) return 12;
         if (std::strcmp(v, "ipmm") != 0) {  // the same schedule as DSL text
             Matrix A2(64, 64, mod), B2(64, 64, mod);
             A2.fill_random(1);

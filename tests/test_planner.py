@@ -103,6 +103,26 @@ def test_error_goldens_through_planner(W):
             W.plan_report(*args)
 
 
+def test_alloc_log_matches_reference(W, O):
+    """CostMeter::alloc_log (meter.hpp:15-19, 40-45): every temporary the plan
+    meters -- words, recursion depth, slot name, in acquisition order -- equals
+    the reference run_variant's log (incl. blocked_acc's scratch chunk and the
+    unmetered QuadrantWorkspace of ipmm)."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    from paper_0707_2347_b200.winomem import last_alloc_log
+    cases = [("std2", 16, 16, 16, 1, 0, 1), ("acc2", 32, 32, 32, 1, 1, 2), ("aclr", 16, 16, 16, 3, 7, 1),
+             ("ovl2", 16, 16, 16, 1, 0, 2), ("acr", 32, 16, 32, 1, 1, 1), ("std2", 64, 32, 16, 1, 0, 4),
+             ("ipmm", 16, 32, 16, 1, 0, 2), ("blocked_acc_t2", 16, 16, 16, 1, 1, 1),
+             ("blocked_acc_t2_acc2", 16, 16, 16, 1, 1, 2), ("ip", 16, 16, 16, 1, 0, 1),
+             ("std2", 1024, 1024, 1024, 1, 0, 128)]
+    for (v, m, k, n, al, be, c) in cases:
+        W.plan_report(v, m, k, n, c, al, be)
+        got = ";".join(f"{w}:{d}:{s}" for w, d, s in last_alloc_log())
+        want = O.ref_alloc_log(v, m, k, n, al, be, c).rstrip(";")
+        assert got == want, (v, m, k, n, c)
+
+
 # SURVEY.md Appendix A / B and 8(d): config-level plans
 CONFIGS = [
     # variant, m, k, n, cutoff, beta, peak words, frames, leaves
