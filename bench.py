@@ -413,10 +413,20 @@ def main():
     import paper_0707_2347_b200 as W
 
     torch.cuda.set_device(local)
-    if world > 1:
+    # WM_BENCH_PARTITION=1: the partitioned path at N = 1 too (a one-rank NCCL
+    # communicator), so the multi-GPU code path is exercised on one GPU
+    if world > 1 or os.environ.get("WM_BENCH_PARTITION") == "1":
+        import socket
         import torch.distributed as dist
         os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if "MASTER_PORT" not in os.environ:
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            sk.close()
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
         run_partitioned(args, cfg, rank, world, local)
         dist.destroy_process_group()
         return
@@ -607,12 +617,14 @@ def run_partitioned(args, cfg, rank, world, local):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    launches0 = be.launches
     with Clocks(local) as clk:
         e0.record()
         for _ in range(args.steps):
             st = step()
         e1.record()
         torch.cuda.synchronize()
+    timed_launches = be.launches - launches0
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3 / args.steps], device=f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -649,7 +661,8 @@ def run_partitioned(args, cfg, rank, world, local):
     dist.all_gather_object(per_rank, {"rank": rank, "products": len(st.products),
                                       "peak_extra_bytes": st.peak_extra_bytes,
                                       "bytes_sent": st.bytes_sent,
-                                      "bytes_received": st.bytes_received})
+                                      "bytes_received": st.bytes_received,
+                                      "timed_launches": timed_launches})
     out = None
     if rank == 0:
         # roofline of the per-rank work: one local product replayed by kernel class
@@ -683,7 +696,7 @@ def run_partitioned(args, cfg, rank, world, local):
             "per_rank": per_rank,
             "peak_extra_bytes_max_rank": max(r["peak_extra_bytes"] for r in per_rank),
             "roofline": roof, "rooflines": rooflines,
-            "gpu_launches": None,
+            "gpu_launches": sum(r["timed_launches"] for r in per_rank),
             "e2e": {"value": 2.0 * m * n * k / e2e_t / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * m * n,
                     "seconds_per_step": e2e_t,

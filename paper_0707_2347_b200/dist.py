@@ -103,6 +103,7 @@ class CudaBackend:
         self.p, self.variant, self.cutoff, self.device, self.real = p, variant, cutoff, device, real
         # REAL64 primitives read the uint32 scalar as a signed int32
         self.m = (1 << 32) if real else p
+        self.launches = 0  # kernels this backend issued (bench.py's gpu_launches)
 
     def _mat(self, t: torch.Tensor):
         return self.W.Matrix.wrap(t, self.W.Modulus(self.p), real=self.real)
@@ -110,21 +111,25 @@ class CudaBackend:
     def lincomb(self, terms):
         out = torch.empty_like(terms[0][1])
         self.W.lincomb(self._mat(out).view(), [(c % self.m, self._mat(b).view()) for c, b in terms])
+        self.launches += 1
         return out
 
     def product(self, X, Y):
         out = torch.empty((X.shape[0], Y.shape[1]), dtype=X.dtype, device=X.device)
         rep = self.W.run_variant(self.variant, self._mat(X), self._mat(Y), self._mat(out),
                                  alpha=1, beta=0, cutoff=self.cutoff)
+        self.launches += rep.n_launches
         return out, rep.peak_extra_bytes
 
     def scale(self, Cq, beta):
         M = self._mat(Cq)
         self.W.block_scale_copy(M.view(), M.view(), beta % self.m)
+        self.launches += 1
 
     def fold(self, Cq, coef, P):
         M = self._mat(Cq)
         self.W.block_addsub(M.view(), M.view(), self._mat(P).view(), 1, coef % self.m)
+        self.launches += 1
 
 
 def product_indices(levels: int) -> List[Tuple[int, ...]]:

@@ -365,7 +365,8 @@ def test_partition_single_rank_gpu(W, O):
                             world_size=1, device_id=torch.device("cuda", 0))
     try:
         for variant, n, cutoff, al, be, lv in [("std2", 512, 64, 1, 0, 1), ("std2", 1024, 128, 3, 7, 1),
-                                               ("ipmm", 512, 64, 1, 0, 1), ("std2", 1024, 64, 3, 7, 2)]:
+                                               ("ipmm", 512, 64, 1, 0, 1), ("std2", 1024, 64, 3, 7, 2),
+                                               ("ip", 1024, 64, 3, 7, 3)]:
             A, B, C = _problem(W, n, n, n, 31 + n, be != 0)
             a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
             be_ = CudaBackend(65521, variant, cutoff, 0)
@@ -576,3 +577,22 @@ def test_context_arena_is_the_schedule_peak(W):
         run("std2", 1024, 128, False)  # plans made before the arena moved are rebuilt
     finally:
         ctx.close()
+
+
+def test_bench_partitioned_path_one_rank():
+    """bench.py's multi-GPU path (run_partitioned) end to end on one GPU through
+    a one-rank NCCL communicator (WM_BENCH_PARTITION=1): the JSON line carries
+    the partition, per-rank peak bytes, e2e, roofline and a passing parity."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WM_BENCH_PARTITION="1")
+    for k_ in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+        env.pop(k_, None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--config", "C1", "--steps", "2",
+                        "--warmup", "1"], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["parity"]["ok"] and line["n_gpus"] == 1
+    assert line["per_rank"][0]["products"] == 7 and line["gpu_launches"] > 0
+    assert line["e2e"]["value"] > 0 and line["roofline"]["peak"]
