@@ -418,7 +418,9 @@ def main():
     if world > 1 or os.environ.get("WM_BENCH_PARTITION") == "1":
         import socket
         import torch.distributed as dist
-        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator size in the log
+        # communicator size in the log -- on stderr: stdout carries only the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if "MASTER_PORT" not in os.environ:
             sk = socket.socket()
             sk.bind(("127.0.0.1", 0))
