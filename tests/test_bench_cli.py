@@ -21,7 +21,15 @@ def _run(args, env_extra):
 def test_gpus_spawns_ranks():
     r = _run(["--gpus", "2"], {})
     assert r.returncode == 0, r.stderr[-2000:]
-    ranks = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    # the ranks share one stdout pipe: their lines may interleave, so decode
+    # every JSON object in the stream rather than line by line
+    dec, ranks, i, out = json.JSONDecoder(), [], 0, r.stdout
+    while True:
+        i = out.find("{", i)
+        if i < 0:
+            break
+        obj, i = dec.raw_decode(out, i)
+        ranks.append(obj)
     assert sorted(x["rank"] for x in ranks) == [0, 1]
     assert all(x["world"] == 2 for x in ranks)
 
