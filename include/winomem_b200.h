@@ -91,9 +91,6 @@ typedef struct {
     uint64_t frame_comb_bytes;
     /* classical leaf flops (2*m*k*n) executed inside fused frames */
     uint64_t frame_leaf_flops;
-    /* fused frames run in quadrant mode: two launches, the product launch chains
-     * each C quadrant's products in its accumulators and writes C itself */
-    uint64_t quad_frames;
 } wm_report;
 
 /* ---- library / context --------------------------------------------------- */
@@ -117,9 +114,6 @@ int wm_ctx_set_stream(wm_ctx* ctx, void* stream);
  *   "dead_hosts" [1]    frame planes in dead blocks (plan liveness)
  *   "cin_direct" [1]    accumulating frames: all planes outside C, C_in read by the combine
  *   "wide_plain" [1]    plain frames' GEMM at BN = 64 (c >= 256)
- *   "quad_frames" [1]   frames with four blocks to spare outside C run as two launches: the
- *                       product launch accumulates each C quadrant over its products
- *                       (no product planes, no combine launch)
  *   "micro" [1]         plans of tiny operations as one launch (shared-memory working set)
  *   "arena_words"       (read-only) words of the context's temporary arena = the largest
  *                       schedule peak run so far (one arena shared by every plan)

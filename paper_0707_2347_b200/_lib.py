@@ -52,8 +52,7 @@ class wm_report(C.Structure):
         "mults", "adds", "peak_extra_words", "total_alloc_words", "word_moves",
         "classical_calls", "schedule_frames", "peak_extra_bytes", "n_ops", "n_launches",
         "fused_frames", "add_bytes", "leaf_flops", "add_bytes_issued", "frame_gemm_bytes",
-        "frame_bytes", "frame_prep_bytes", "frame_comb_bytes", "frame_leaf_flops",
-        "quad_frames")]
+        "frame_bytes", "frame_prep_bytes", "frame_comb_bytes", "frame_leaf_flops")]
 
 
 _lib = None

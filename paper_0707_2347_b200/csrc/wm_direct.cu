@@ -349,224 +349,6 @@ __global__ void __launch_bounds__(NT, 1)
     if (tid == 32) WM_DSTAMP(7);
 }
 
-// ---- quadrant mode -----------------------------------------------------------
-//
-// U1 = P1 + P2, U5 = P1 + P6 + P5 + P3, U6 = P1 + P6 + P7 - P4, U7 = P1 + P6 + P7 + P5:
-// every C quadrant of a Winograd frame is a sum of products, i.e. ONE product
-// over the concatenated K ranges of its terms (with p - A22 standing in for A22).
-// A pair of CTAs (a cluster of two) owns a 128 x BN tile of one quadrant; each
-// CTA streams the operand panels of half of that quadrant's 2 or 4 products
-// through its ring into its own four limb accumulators (each <= 2 k 255^2 <
-// 2^31) and reduces its partial sum mod p.  The two then swap halves through
-// distributed shared memory -- CTA 0 finishes rows [0, 64), CTA 1 rows [64, 128)
-// -- and write C = alpha * (r0 + r1) + beta * C_in as float64 residues.  So the
-// products never exist in memory and the combine is the epilogue.  It costs
-// twice the tensor work of the seven separate products (14 K ranges instead of
-// 7) on a pipe that is ~7% busy, and saves the product planes' round trip and a
-// launch on the frame's critical chain.
-__constant__ int kQuadSeg[4][4] = {{0, 1, -1, -1}, {0, 5, 4, 2}, {0, 5, 6, 3}, {0, 5, 6, 4}};
-
-template <int BN>
-struct QSmem {
-    DSmem<BN> d;
-    alignas(16) std::uint16_t xch[BM / 2][BN];  // the partner's residues of the rows this CTA finishes
-};
-
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-
-template <int BN>
-__global__ void __launch_bounds__(NT, 1)
-    k_gemm_quads(const __grid_constant__ GemmParams P, const __grid_constant__ TmaMaps M) {
-    using C = DCfg<BN>;
-    constexpr int NS = C::NS;
-    extern __shared__ std::uint8_t smem_raw[];
-    const std::uint32_t base = tc::smem_u32(smem_raw);
-    QSmem<BN>& Q = *reinterpret_cast<QSmem<BN>*>(smem_raw + ((1024 - (base & 1023)) & 1023));
-    DSmem<BN>& S = Q.d;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const std::uint32_t rank = blockIdx.x;  // rank in the CTA pair (cluster dims 2 x 1 x 1)
-    // heavy quadrants first: blockIdx.z = (3 - quadrant) * tiles_m + row tile
-    const int quad = 3 - static_cast<int>(blockIdx.z / P.tiles_m);
-    const std::uint32_t i0 = (blockIdx.z % P.tiles_m) * BM;
-    const std::uint32_t j0 = blockIdx.y * BN;
-    const int nseg = quad == 0 ? 1 : 2;  // products per CTA
-    const int seg0 = static_cast<int>(rank) * nseg;
-    const std::uint32_t nkc = P.k / KT, nk = nkc * nseg;
-
-    if (tid == 32) WM_DSTAMP(0);
-    if (warp == 0) tc::tmem_alloc(&S.tmem_base, C::TCOLS);
-    if (tid == 32) {
-        for (int s = 0; s < NS; ++s) {
-            tc::mbar_init(&S.full[s], 1);
-            tc::mbar_init(&S.empty[s], 1);
-        }
-        tc::mbar_init(&S.done, 1);
-        tc::mbar_fence_init();
-    }
-    tc::fence_before();
-    __syncthreads();
-    tc::fence_after();
-    cluster_sync_all();  // the partner is resident before anyone writes into its shared memory
-    const std::uint32_t tbase = S.tmem_base;
-    if (tid == 32) WM_DSTAMP(1);
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    WM_PDL_EARLY_C();
-    WM_TL_BEGIN(P.tl);
-    if (tid == 32) WM_DSTAMP(2);
-
-    if (warp == 0) {
-        if (lane == 0) {
-            constexpr std::uint32_t bytes = 2 * A_PART + 2 * C::B_PART;
-            for (std::uint32_t kc = 0; kc < nk; ++kc) {
-                const int st = kc % NS;
-                if (kc >= static_cast<std::uint32_t>(NS))
-                    tc::mbar_wait(&S.empty[st], ((kc / NS) - 1) & 1);
-                tc::mbar_arrive_expect_tx(&S.full[st], bytes);
-                const int prod = kQuadSeg[quad][seg0 + kc / nkc];
-                const int k0 = static_cast<int>((kc % nkc) * KT);
-                tma_load_3d(S.stage[st], &M.a[prod], k0, static_cast<int>(i0), 0, &S.full[st]);
-                tma_load_3d(S.stage[st] + 2 * A_PART, &M.b[prod], static_cast<int>(j0), k0, 0,
-                            &S.full[st]);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        constexpr std::uint32_t idesc = idesc_direct(BM, 2 * BN);
-        for (std::uint32_t kc = 0; kc < nk; ++kc) {
-            const int st = kc % NS;
-            tc::mbar_wait(&S.full[st], (kc / NS) & 1);
-            tc::fence_after();
-            if (lane == 0 && kc == 0) WM_DSTAMP(3);
-            if (lane == 0 && kc + 1 == nk) WM_DSTAMP(4);
-            if (lane == 0) {
-                const std::uint32_t sa = tc::smem_u32(S.stage[st]);
-                const std::uint32_t sb = sa + 2 * A_PART;
-#pragma unroll
-                for (int s = 0; s < KT / 32; ++s) {
-                    const std::uint64_t ah = sdesc(sa + s * 32, 16, 8 * KT, A_LAYOUT);
-                    const std::uint64_t al = sdesc(sa + A_PART + s * 32, 16, 8 * KT, A_LAYOUT);
-                    const std::uint64_t b = sdesc(sb + s * 32 * BN, C::B_PART, 8 * BN, C::B_LAYOUT);
-                    const bool acc = kc > 0 || s > 0;
-                    tc::mma_i8(tbase + 0, ah, b, idesc, acc);
-                    tc::mma_i8(tbase + 2 * BN, al, b, idesc, acc);
-                }
-                tc::commit(&S.empty[st]);
-                if (kc + 1 == nk) tc::commit(&S.done);
-            }
-            __syncwarp();
-        }
-    }
-    WM_PDL_LATE_C();
-
-    // eight epilogue warps: TMEM lane quarter = warp % 4 (rows 32 lg ..), column
-    // half = (warp - 2) / 4.  Rows [64 rank, 64 rank + 64) are finished here; the
-    // residues of the other rows go to the partner.
-    const int lg = warp & 3, half = (warp - 2) >> 2;
-    const bool mine = warp >= 2 && static_cast<std::uint32_t>(lg >> 1) == rank;
-    const std::uint32_t row = lg * 32 + lane;
-    constexpr int NQ = BN / 32;  // 16-column groups per thread
-    const double p = P.pd, pinv = P.pinv;
-    const std::uint32_t pi = static_cast<std::uint32_t>(p);
-    std::uint32_t res[NQ][16];
-    double* crow = P.cq[quad] + static_cast<std::uint64_t>(i0 + row) * P.cld + j0 + half * (BN / 2);
-    // C_in of this thread's columns, requested while the products run (narrow tiles)
-    constexpr bool PRE = NQ <= 2;
-    double2 cin[PRE ? NQ : 1][8];
-    if (warp >= 2) {
-        if (PRE && mine && P.beta != 0) {
-#pragma unroll
-            for (int q = 0; q < (PRE ? NQ : 1); ++q)
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    cin[q][e] = *reinterpret_cast<const double2*>(crow + q * 16 + 2 * e);
-        }
-        tc::mbar_wait(&S.done, 0);
-        tc::fence_after();
-        if (tid == 64) WM_DSTAMP(5);
-        const std::uint32_t lane_off = static_cast<std::uint32_t>(lg * 32) << 16;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            tmem_cols16<BN>(tbase + lane_off + half * (BN / 2) + q * 16, res[q], p, pinv, pi);
-        if (!mine) {
-            // into the partner's exchange rows
-            std::uint32_t peer;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
-                         : "=r"(peer)
-                         : "r"(tc::smem_u32(&Q.xch[row & 63][half * (BN / 2)])), "r"(rank ^ 1u));
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                std::uint32_t w[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) w[e] = res[q][2 * e] | (res[q][2 * e + 1] << 16);
-                asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(peer + q * 32),
-                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
-                             : "memory");
-                asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};\n" ::"r"(peer + q * 32 + 16),
-                             "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-                             : "memory");
-            }
-        }
-    }
-    cluster_sync_all();  // both halves' residues have been exchanged
-    if (mine) {
-        if (tid == 64 || tid == 128) WM_DSTAMP(8);
-        const bool plain = P.alpha == 1 && P.beta <= 1;
-        const double al = static_cast<double>(P.alpha), be = static_cast<double>(P.beta);
-        const std::uint16_t* xr = &Q.xch[row & 63][half * (BN / 2)];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            if (!PRE && P.beta != 0) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    cin[0][e] = *reinterpret_cast<const double2*>(crow + q * 16 + 2 * e);
-            }
-            const uint4 x0 = *reinterpret_cast<const uint4*>(xr + q * 16);
-            const uint4 x1 = *reinterpret_cast<const uint4*>(xr + q * 16 + 8);
-            const std::uint32_t xw[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                double v[2];
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    std::uint32_t r = res[q][2 * e + h] + (h ? xw[e] >> 16 : xw[e] & 0xFFFFu);
-                    r = r >= pi ? r - pi : r;
-                    const double2 ce = cin[PRE ? q : 0][e];
-                    const double c = h ? ce.y : ce.x;
-                    if (plain) {
-                        // alpha = 1, beta in {0, 1}: residue + canonical C_in, one fold
-                        if (P.beta != 0) {
-                            r += static_cast<std::uint32_t>(c);
-                            r = r >= pi ? r - pi : r;
-                        }
-                        v[h] = u2d(r);
-                    } else {
-                        double x = reduce_modp(al * u2d(r), p, pinv);  // alpha r < 2^32
-                        if (P.beta != 0) x = reduce_modp(fma(be, c, x), p, pinv);  // < 2^33
-                        v[h] = x;
-                    }
-                }
-                *reinterpret_cast<double2*>(crow + q * 16 + 2 * e) = make_double2(v[0], v[1]);
-            }
-        }
-        if (tid == 64 || tid == 128) WM_DSTAMP(6);
-    }
-
-    tc::fence_before();
-    __syncthreads();
-    WM_TL_END(P.tl);
-    if (warp == 0) tc::tmem_dealloc(tbase, C::TCOLS);
-    if (tid == 32) WM_DSTAMP(7);
-}
-
-template <int BN>
-constexpr std::size_t qsmem_bytes() {
-    static_assert(sizeof(QSmem<BN>) + 1024 <= 232448, "shared memory budget");
-    return sizeof(QSmem<BN>) + 1024;
-}
-
 template <int BN>
 constexpr std::size_t dsmem_bytes() {
     static_assert(sizeof(DSmem<BN>) + 1024 <= 232448, "shared memory budget");
@@ -592,31 +374,6 @@ cudaError_t dlaunch(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k_gemm_direct<BN, BSRC>, P, M);
-}
-
-template <int BN>
-cudaError_t qlaunch(const GemmParams& P, const TmaMaps& M, cudaStream_t s) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2, P.n / BN, P.tiles_m * 4);  // x: the CTA pair of one tile
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = qsmem_bytes<BN>();
-    cfg.stream = s;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = 2;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, k_gemm_quads<BN>, P, M);
-}
-
-template <int BN>
-cudaError_t qset_attr() {
-    return cudaFuncSetAttribute(k_gemm_quads<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(qsmem_bytes<BN>()));
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 g_denc = nullptr;
@@ -653,9 +410,6 @@ cudaError_t gemm_direct_init() {
     if ((e = dset_attr<128, 0>()) != cudaSuccess) return e;
     if ((e = dset_attr<32, 1>()) != cudaSuccess) return e;
     if ((e = dset_attr<64, 1>()) != cudaSuccess) return e;
-    if ((e = qset_attr<32>()) != cudaSuccess) return e;
-    if ((e = qset_attr<64>()) != cudaSuccess) return e;
-    if ((e = qset_attr<128>()) != cudaSuccess) return e;
     g_direct_ok = true;
     return cudaSuccess;
 }
@@ -703,34 +457,6 @@ int gemm_direct_choose(const GemmParams& P) {
     for (int bn : {32, 64, 128})
         if (bn <= widest && P.n % bn == 0 && mt * (P.n / bn) <= 148) return bn;
     return P.n % widest == 0 ? widest : P.n % 64 == 0 ? 64 : 32;
-}
-
-// Quadrant mode: seven plane-pair products of one square shape, limb
-// accumulators of four chained products within int32 (k <= 8192).
-bool gemm_quads_supported(const GemmParams& P, int bn) {
-    if (!gemm_direct_supported(P, bn) || bn >= 1000 || P.nprod != 7 || P.k > 16384) return false;
-    for (std::uint32_t i = 0; i < 7; ++i)
-        if (P.b[i].fmt != 2) return false;
-    for (int q = 0; q < 4; ++q)
-        if (!P.cq[q] || (reinterpret_cast<std::uintptr_t>(P.cq[q]) & 15u)) return false;
-    return P.cld % 2 == 0;
-}
-
-// the narrowest tile whose grid (4 quadrants x row tiles x column tiles, two CTAs
-// each) fits one wave
-int gemm_quads_choose(const GemmParams& P) {
-    for (int bn : {32, 64, 128})
-        if (P.n % bn == 0 && 8 * P.tiles_m * (P.n / bn) <= 148) return bn;
-    return P.n % 128 == 0 ? 128 : P.n % 64 == 0 ? 64 : 32;
-}
-
-cudaError_t launch_gemm_quads(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s) {
-    switch (bn) {
-        case 32: return qlaunch<32>(P, M, s);
-        case 64: return qlaunch<64>(P, M, s);
-        case 128: return qlaunch<128>(P, M, s);
-        default: return cudaErrorInvalidValue;
-    }
 }
 
 // bn: 32 / 64; + 1000 selects cp.async B loads instead of TMA

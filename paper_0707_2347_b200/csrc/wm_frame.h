@@ -39,7 +39,6 @@ struct FramePrepParams {
     std::uint32_t limbs;             // 1: limb-pair planes (hi bytes [0,c), lo [c,2c) per row)
     std::uint32_t c;                 // quadrant size
     std::uint32_t beta;              // accumulate: pack beta*C_in into C11 slots
-    std::uint32_t neg_a22;           // the A22 plane holds p - A22 (quadrant-mode GEMM: U6 as a sum)
     double pd, pinv;
     unsigned long long* tl;          // measurement timeline slot (nullptr: off)
 };

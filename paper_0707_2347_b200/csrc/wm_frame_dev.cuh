@@ -135,12 +135,7 @@ __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::
     }
     put(PL_A11, a11);
     put(PL_A12, a12);
-    if (P.neg_a22) {
-        const double n22[2] = {a22[0] == 0.0 ? 0.0 : p - a22[0], a22[1] == 0.0 ? 0.0 : p - a22[1]};
-        put(PL_A22, n22);
-    } else {
-        put(PL_A22, a22);
-    }
+    put(PL_A22, a22);
     put(PL_B11, b11);
     put(PL_B21, b21);
     put(PL_B22, b22);

@@ -28,11 +28,6 @@ struct GemmParams {
     double pd, pinv;
     unsigned long long* trace;  // diagnostics: per-CTA phase timestamps (nullptr: off)
     unsigned long long* tl;     // measurement timeline slot (nullptr: off)
-    // Quadrant mode of the direct engine (launch_gemm_quads): the launch writes the
-    // four C quadrants of a Winograd frame, C_q = alpha * U_q + beta * C_q, each
-    // output tile accumulating its U_q over the products that make it up.
-    double* cq[4];
-    std::uint64_t cld;
 };
 
 // TMA operand maps (one pair per product), encoded on the host at lowering time
@@ -56,13 +51,5 @@ bool gemm_direct_supported(const GemmParams& P, int bn);
 bool gemm_direct_encode(const GemmParams& P, int bn, TmaMaps& M);
 int gemm_direct_choose(const GemmParams& P);
 cudaError_t launch_gemm_direct(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s);
-// Quadrant mode: the seven operand pairs are those of P1..P7 with a[3] holding
-// p - A22 (so that every term of the U-chain is a sum); one CTA per (quadrant,
-// 128 x BN tile) chains the K ranges of its quadrant's products into one set of
-// accumulators -- C11: P1 P2, C12: P1 P6 P5 P3, C21: P1 P6 P7 P4', C22: P1 P6 P7 P5
-// -- and writes float64 residues straight into C.  No product planes, no combine.
-bool gemm_quads_supported(const GemmParams& P, int bn);
-int gemm_quads_choose(const GemmParams& P);
-cudaError_t launch_gemm_quads(const GemmParams& P, const TmaMaps& M, int bn, cudaStream_t s);
 
 }  // namespace wm

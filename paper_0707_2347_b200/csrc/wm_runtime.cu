@@ -75,7 +75,6 @@ struct Step {
     FrameCombParams fcomb;
     int engine = 0;         // int8 GEMM: 0 cp.async, 1 TMA
     int bn = 32, split = 1;
-    bool to_c = false;  // FGEMM (direct engine, quadrant mode): writes the C quadrants, no combine
     std::shared_ptr<TmaMaps> tmaps;
     unsigned long long* tl = nullptr;  // GROUP: measurement timeline slot
     // UPLOAD / DOWNLOAD (host u32 boundary): one block of a host matrix, staged
@@ -123,10 +122,6 @@ void frame_sets(const Op& o, const Field& f, std::vector<Step>& steps, std::size
             if (s.kind == Step::FPREP) {
                 add(s.rd, o.a), add(s.rd, o.b);
                 for (int e = 0; e < 4; ++e) add(s.wr, ext[e]);
-            } else if (s.kind == Step::FGEMM && s.to_c) {
-                for (int e = 0; e < 4; ++e) add(s.rd, ext[e]);
-                if (acc) add(s.rd, o.d);
-                add(s.wr, o.d);
             } else if (s.kind == Step::FGEMM) {
                 for (int e = 0; e < 4; ++e) add(s.rd, ext[e]);
                 add(s.wr, o.h0), add(s.wr, o.h1);
@@ -224,8 +219,6 @@ struct wm_ctx {
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
     bool cin_direct = true;     // accumulating frames: all planes in dead blocks, C_in read by the combine
-    bool quad_frames = true;    // frames with four blocks to spare outside C: the product launch
-                                // writes the C quadrants (quadrant mode), no product planes, no combine
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
     const void* traced = nullptr;  // CachedPlan of the last traced run
     Lanes lanes;
@@ -434,8 +427,7 @@ void finish_gemm_step(Step& st, int engine, int force = 0) {
 
 // A fused leaf frame -> prep / seven-product GEMM / combine launches.
 void lower_frame(const Op& op, const Field& f, double* const base[4], std::vector<Step>& steps,
-                 int engine, bool direct, bool wide_plain, const View* ext = nullptr,
-                 bool quads = false) {
+                 int engine, bool direct, bool wide_plain, const View* ext = nullptr) {
     const int force = 0;
     const std::uint64_t c = op.a.rows / 2;
     auto ptr = [&](const View& v) { return base[v.region] + v.off; };
@@ -551,28 +543,6 @@ void lower_frame(const Op& op, const Field& f, double* const base[4], std::vecto
     G.beta = 0;
     G.pd = pd;
     G.pinv = pinv;
-    if (direct && quads && ext) {
-        // quadrant mode: every plane lives outside C (ext), the product launch
-        // chains each quadrant's products in its accumulators and writes C itself
-        for (int i = 0; i < 4; ++i) G.cq[i] = ptr(cq[i]);
-        G.cld = op.d.ld;
-        G.alpha = op.sa.r;
-        G.beta = op.sb.r;
-        g.bn = gemm_quads_choose(G);
-        auto maps = std::make_shared<TmaMaps>();
-        if (gemm_quads_supported(G, g.bn) && gemm_direct_encode(G, g.bn, *maps)) {
-            steps.back().fprep.neg_a22 = 1;  // U6 = U3 + (p - A22) T4
-            g.tmaps = maps;
-            g.engine = 2;
-            g.split = 1;
-            g.to_c = true;
-            steps.push_back(g);
-            return;
-        }
-        std::memset(G.cq, 0, sizeof(G.cq));
-        G.alpha = 1;
-        G.beta = 0;
-    }
     if (direct) {
         g.bn = (force >= 1000 && force < 3000) ? force % 1000 + 1000 * (force / 1000 - 1)
                                                 : gemm_direct_choose(G);
@@ -978,31 +948,15 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
             Op fop = op;  // product (and raw) planes in dead blocks when there are some
             View ext[4];
             bool use_ext = false;
-            const bool direct = ctx.direct_ok && ctx.direct_frames;
-            bool quads = false;
             if (ctx.dead_hosts && op.frame >= 0) {
                 // accumulating frames: a third block takes the raw planes, so that
                 // with two temporaries B22 is materialised too and the GEMM no
                 // longer reads the frame's B (the parent's next prep rewrites it)
                 const bool acc = !f.is_zero(op.sb);
-                const bool want_quads = ctx.quad_frames && direct && op.a.rows / 2 <= 2048;
                 const std::vector<View> w =
                     choose_product_hosts(plan, oi, fold ? &folds[oi] : nullptr, by_frame[op.frame],
-                                         recent_hosts, want_quads ? (acc ? 6 : 4) : acc ? 6 : 2,
-                                         access_ix);
-                // quadrant mode needs four blocks outside C for the fourteen operand
-                // planes and none for products: dead blocks first (no sibling frame
-                // touches them), then the frame's own temporaries
-                std::vector<View> four(w.begin(), w.begin() + std::min<std::size_t>(4, w.size()));
-                if (want_quads)
-                    for (const View* h : {&op.h0, &op.h1, &op.h2})
-                        if (four.size() < 4 && h->rows == op.a.rows / 2 && h->cols == op.a.rows / 2 &&
-                            h->ld % 2 == 0)
-                            four.push_back(*h);
-                if (want_quads && four.size() == 4) {
-                    for (int e = 0; e < 4; ++e) ext[e] = four[e];
-                    use_ext = quads = true;
-                } else if (w.size() >= 2) {
+                                         recent_hosts, acc ? 6 : 2, access_ix);
+                if (w.size() >= 2) {
                     fop.h0 = w[0];
                     fop.h1 = w[1];
                     if (acc && w.size() >= 6 && ctx.cin_direct) {
@@ -1015,19 +969,15 @@ std::vector<Step> lower(const Plan& plan, double* const base[4], const wm_ctx& c
                 }
                 // the next frames keep off the plane hosts of the last `keep` frames
                 const std::size_t keep = 2;  // launch-DAG model: 2 beats 1, 3, 4
-                if (quads) {
-                    host_hist.push_back(std::vector<View>(ext, ext + 4));
-                } else {
-                    host_hist.push_back({fop.h0, fop.h1});
-                    if (fop.h2.rows) host_hist.back().push_back(fop.h2);
-                    if (use_ext) host_hist.back().insert(host_hist.back().end(), ext, ext + 4);
-                }
+                host_hist.push_back({fop.h0, fop.h1});
+                if (fop.h2.rows) host_hist.back().push_back(fop.h2);
+                if (use_ext) host_hist.back().insert(host_hist.back().end(), ext, ext + 4);
                 while (host_hist.size() > keep) host_hist.erase(host_hist.begin());
                 recent_hosts.clear();
                 for (const auto& hv : host_hist) recent_hosts.insert(recent_hosts.end(), hv.begin(), hv.end());
             }
-            lower_frame(fop, f, base, steps, ctx.gemm_engine, direct, ctx.wide_plain,
-                        use_ext ? ext : nullptr, quads);
+            lower_frame(fop, f, base, steps, ctx.gemm_engine, ctx.direct_ok && ctx.direct_frames,
+                        ctx.wide_plain, use_ext ? ext : nullptr);
             frame_sets(fop, f, steps, first, use_ext ? ext : nullptr);
             if (fold && (folds[oi].op[0] >= 0 || folds[oi].op[1] >= 0))
                 for (std::size_t j = first; j < steps.size(); ++j)
@@ -1102,8 +1052,7 @@ void issue_one(const Step& s, bool real, cudaStream_t st, const Step* prev = nul
         case Step::GROUP: WM_CUDA(launch_group(s.gid, s.grp, real, st, s.tl)); break;
         case Step::FPREP: WM_CUDA(launch_frame_prep(s.fprep, st)); break;
         case Step::FGEMM:
-            if (s.engine == 2 && s.to_c) WM_CUDA(launch_gemm_quads(s.fgemm, *s.tmaps, s.bn, st));
-            else if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
+            if (s.engine == 2) WM_CUDA(launch_gemm_direct(s.fgemm, *s.tmaps, s.bn, st));
             else if (s.engine == 1) WM_CUDA(launch_gemm_tma(s.fgemm, *s.tmaps, s.bn, s.split, st));
             else WM_CUDA(launch_gemm_i8(s.fgemm, st));
             break;
@@ -1287,13 +1236,6 @@ void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r)
                                     kn = static_cast<std::uint64_t>(G.k) * G.n,
                                     mn = static_cast<std::uint64_t>(G.m) * G.n;
                 r->frame_leaf_flops += 2ull * G.m * G.k * G.n * G.nprod;
-                if (s.to_c) {
-                    // 14 operand panel pairs (C11: 2 products, the others 4), C written
-                    // (and C_in read) as float64
-                    r->frame_gemm_bytes += 14 * (mk + kn) * 2 + 4 * mn * 8 * (G.beta ? 2 : 1);
-                    ++r->quad_frames;
-                    continue;
-                }
                 for (std::uint32_t i = 0; i < G.nprod; ++i)
                     r->frame_gemm_bytes += mk * (G.a[i].fmt != 0 ? 2 : 8) +
                                            kn * (G.b[i].fmt != 0 ? 2 : 8) +
@@ -1520,7 +1462,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->micro << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << ctx->quad_frames << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->micro << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1842,7 +1784,6 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "wide_plain") ctx->wide_plain = value != 0;
         else if (k == "cin_direct") ctx->cin_direct = value != 0;
-        else if (k == "quad_frames") ctx->quad_frames = value != 0;
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -1872,7 +1813,6 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;
         else if (k == "cin_direct") *value = ctx->cin_direct;
-        else if (k == "quad_frames") *value = ctx->quad_frames;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else fail(E_INVALID, "unknown option " + k);

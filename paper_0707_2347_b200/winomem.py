@@ -167,7 +167,6 @@ class CostReport:
     frame_prep_bytes: int = 0
     frame_comb_bytes: int = 0
     frame_leaf_flops: int = 0
-    quad_frames: int = 0
 
     def ops(self):
         return self.mults + self.adds
@@ -208,7 +207,7 @@ def _report(variant, m, k, n, cutoff, r: wm_report) -> CostReport:
                       r.total_alloc_words, r.word_moves, r.classical_calls, calls,
                       r.peak_extra_bytes, r.n_ops, r.n_launches, r.fused_frames, r.add_bytes,
                       r.leaf_flops, r.add_bytes_issued, r.frame_gemm_bytes, r.frame_bytes,
-                      r.frame_prep_bytes, r.frame_comb_bytes, r.frame_leaf_flops, r.quad_frames)
+                      r.frame_prep_bytes, r.frame_comb_bytes, r.frame_leaf_flops)
 
 
 # ---- device context ------------------------------------------------------

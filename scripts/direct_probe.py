@@ -20,7 +20,7 @@ ctx = W.Context(p=65521)
 res = {}
 for c in (128, 256, 512):
     for bn in (32, 64, 128):
-        for bconv in (0, 1, 2):  # 2: quadrant mode (C written by the product launch)
+        for bconv in (0, 1):
             bad = C.c_uint64()
             us = C.c_double()
             tr = np.zeros((c // 128) * 7 * (c // (bn % 1000)) * 16, dtype=np.uint64)
@@ -31,11 +31,6 @@ for c in (128, 256, 512):
             if rc:
                 res[key]["err"] = L.wm_last_error().decode() if hasattr(L, "wm_last_error") else ""
             t = tr.reshape(-1, 16).astype(np.int64)
-            if bconv == 2:  # four quadrants' CTAs instead of seven products'
-                t = t[:(c // 128) * 4 * (c // bn)]
-            if rc:
-                print(key, res[key], flush=True)
-                continue
             t0 = t[:, 0].min()
             names = ["start", "init", "gdc", "full0", "full_last", "done", "stored", "end"]
             res[key]["trace_med"] = {nm: round(float(np.median(t[:, i] - t0)) / 1000, 2)

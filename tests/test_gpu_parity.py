@@ -44,17 +44,15 @@ def golden():
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
                         dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
                         dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0),
-                        dict(fold=0), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0),
-                        dict(quad_frames=0)],
+                        dict(fold=0), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0)],
                 ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync", "convert-frames",
-                     "one-stream", "no-fold", "no-dead-hosts", "narrow-plain", "packed-cin",
-                     "three-launch-frames"])
+                     "one-stream", "no-fold", "no-dead-hosts", "narrow-plain", "packed-cin"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
                                               "leaf_kernel", "fuse_adds", "gemm_engine",
                                               "direct_frames", "dag", "fold", "dead_hosts",
-                                              "wide_plain", "cin_direct", "quad_frames")}
+                                              "wide_plain", "cin_direct")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
