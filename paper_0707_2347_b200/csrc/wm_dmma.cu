@@ -186,10 +186,12 @@ cudaError_t launch_cfg(const MulParams& P, cudaStream_t s) {
 // the grid is several waves deep (31.7 TFLOP/s at 2048^3 in isolation); a 1024^3
 // leaf is only 256 tiles on 148 SMs (20 TFLOP/s alone), but inside a
 // multiplication the lanes overlap neighbouring leaves and this shape wins.
-// Measured and dropped (profiles/r2/dmma_sweep.log): 128 x 64, 64 x 128 and
-// 128 x 128 tiles, three- and four-stage rings, and two or four warp groups
-// splitting the k steps of a tile (23.7 TFLOP/s on a lone 1024^3 leaf, but config 5
-// 1650 vs 1570 ms).
+// Measured inside config 5, whose 2-temporary schedule runs its 16,807 leaves
+// strictly one after another (profiles/r2/dmma_c5_bench.txt; this shape 1570 ms):
+// 64 x 32 tiles 1616, 32 x 64 1650, 128 x 64 1680, 64 x 128 1712, 32 x 32 2365,
+// 128 x 128 2942-3044, a three-stage ring 1567 (no difference), two warp groups
+// splitting the k steps of a tile 1650 (faster on a lone leaf in a replay loop,
+// profiles/r2/dmma_sweep.log, slower in the real chain).
 template <bool REAL, bool VEC>
 cudaError_t launch_shape(const MulParams& P, cudaStream_t s) {
     return launch_cfg<REAL, 64, 64, 2, 2, 2, VEC>(P, s);

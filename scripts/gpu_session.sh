@@ -1,5 +1,4 @@
-timeout 1200 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "real64 or unfused-dmma or primitive or classical_vs" > gpurun_out/pytest_gpu_a.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu_a.log
-for o in dmma_shape=0 dmma_shape=1; do
+for o in dmma_shape=1 dmma_shape=2 dmma_shape=3 dmma_shape=5; do
 echo "== C5 $o"
 WM_OPTS=$o timeout 900 python bench.py --config C5 --steps 3 --warmup 3 2> gpurun_out/bench_err.log | python -c "
 import json,sys
