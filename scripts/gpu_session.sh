@@ -1,4 +1,4 @@
-for o in dmma_shape=1 dmma_shape=2 dmma_shape=3 dmma_shape=5; do
+for o in dmma_spread=2 dmma_spread=1; do
 echo "== C5 $o"
 WM_OPTS=$o timeout 900 python bench.py --config C5 --steps 3 --warmup 3 2> gpurun_out/bench_err.log | python -c "
 import json,sys

@@ -73,6 +73,7 @@ def main():
     # into the gap before its first CTA started and its own span
     j = int(np.argmax(end))
     crit, gaps, edges = {}, {}, {}
+    lane_edges = {"same": [0, 0.0], "cross": [0, 0.0]}  # critical edges: count, gap us
     path = 0
     while j >= 0:
         preds = [p for p in [prev_on_lane[j]] + [w for w in waits[j] if w >= 0] if p >= 0]
@@ -83,6 +84,10 @@ def main():
         edges[e_] = edges.get(e_, 0) + 1
         crit[k_] = crit.get(k_, 0.0) + end[j] - max(start[j], pe)
         gaps[k_] = gaps.get(k_, 0.0) + max(0.0, start[j] - pe)
+        if p >= 0:
+            le = lane_edges["same" if lane[p] == lane[j] else "cross"]
+            le[0] += 1
+            le[1] += max(0.0, start[j] - pe)
         path += 1
         j = p
     span = {}
@@ -101,6 +106,8 @@ def main():
                       "critical_span_us_by_kind": {k_: round(v, 1) for k_, v in crit.items()},
                       "critical_gap_us_by_kind": {k_: round(v, 1) for k_, v in gaps.items()},
                       "span_stats": stats,
+                      "critical_edges_by_lane": {k_: {"n": v[0], "gap_us": round(v[1], 1)}
+                                                 for k_, v in lane_edges.items()},
                       "critical_edges": dict(sorted(edges.items(), key=lambda kv: -kv[1])[:12]),
                       "lanes": {int(l): int((lane == l).sum()) for l in np.unique(lane)}}))
 
