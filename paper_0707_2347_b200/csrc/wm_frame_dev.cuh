@@ -26,6 +26,27 @@ __device__ __forceinline__ double subm(double a, double b, double p) {
     return v < 0.0 ? v + p : v;
 }
 
+// canonical residue (an integer < 2^32 held in a float64) -> uint32 and back
+// without conversion instructions: 2^52 + x keeps x in its low mantissa word
+__device__ __forceinline__ std::uint32_t d2u(double x) {
+    return static_cast<std::uint32_t>(__double2loint(x + 4503599627370496.0));
+}
+__device__ __forceinline__ double u2d(std::uint32_t u) {
+    return __hiloint2double(0x43300000, static_cast<int>(u)) - 4503599627370496.0;
+}
+// residues on the integer pipe: a, b < p < 2^16
+__device__ __forceinline__ std::uint32_t addp(std::uint32_t a, std::uint32_t b, std::uint32_t p) {
+    const std::uint32_t v = a + b;
+    return v >= p ? v - p : v;
+}
+__device__ __forceinline__ std::uint32_t subp(std::uint32_t a, std::uint32_t b, std::uint32_t p) {
+    return a >= b ? a - b : a + p - b;
+}
+__device__ __forceinline__ std::uint32_t fold4(std::uint32_t v, std::uint32_t p) {  // v < 4p
+    v = v >= 2 * p ? v - 2 * p : v;
+    return v >= p ? v - p : v;
+}
+
 __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
     const double2 a = *reinterpret_cast<const double2*>(p);
     const double2 b = *reinterpret_cast<const double2*>(p + 2);
@@ -100,52 +121,60 @@ __device__ __forceinline__ void prep_limbs_load(const FramePrepParams& P, std::u
 
 __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::uint64_t r,
                                                  std::uint64_t j, const PrepRegs& R) {
-    const double p = P.pd;
     store_operand(P.A, P.fold[0], r, j, R.av);
     store_operand(P.B, P.fold[1], r, j, R.bv);
-    const double(&a11)[2] = R.av[0], (&a12)[2] = R.av[1], (&a21)[2] = R.av[2], (&a22)[2] = R.av[3];
-    const double(&b11)[2] = R.bv[0], (&b12)[2] = R.bv[1], (&b21)[2] = R.bv[2], (&b22)[2] = R.bv[3];
-    double s[4][2], t[4][2];
+    // S / T on the integer pipe (the float64 pipe is the narrow one on this part)
+    const std::uint32_t p = static_cast<std::uint32_t>(P.pd);
+    std::uint32_t a[4][2], b[4][2];  // quadrants 11, 12, 21, 22
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            a[k][e] = d2u(R.av[k][e]);
+            b[k][e] = d2u(R.bv[k][e]);
+        }
+    std::uint32_t s[4][2], t[4][2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-        const double s1 = addm(a21[e], a22[e], p), s2 = subm(s1, a11[e], p);
+        const std::uint32_t s1 = addp(a[2][e], a[3][e], p), s2 = subp(s1, a[0][e], p);
         s[0][e] = s1;
         s[1][e] = s2;
-        s[2][e] = subm(a11[e], a21[e], p);
-        s[3][e] = subm(a12[e], s2, p);
-        const double t1 = subm(b12[e], b11[e], p), t2 = subm(b22[e], t1, p);
+        s[2][e] = subp(a[0][e], a[2][e], p);
+        s[3][e] = subp(a[1][e], s2, p);
+        const std::uint32_t t1 = subp(b[1][e], b[0][e], p), t2 = subp(b[3][e], t1, p);
         t[0][e] = t1;
         t[1][e] = t2;
-        t[2][e] = subm(b22[e], b12[e], p);
-        t[3][e] = subm(t2, b21[e], p);
+        t[2][e] = subp(b[3][e], b[1][e], p);
+        t[3][e] = subp(t2, b[2][e], p);
     }
     const std::uint32_t c = P.c;
-    auto put = [&](int pl, const double (&v)[2]) {
+    // two residues -> their high bytes / their low bytes, one byte permute each
+    auto put = [&](int pl, const std::uint32_t (&v)[2]) {
         if (!P.plane[pl]) return;
         std::uint8_t* row = static_cast<std::uint8_t*>(P.plane[pl]) + r * P.pld[pl];
-        const std::uint32_t x0 = static_cast<std::uint32_t>(v[0]), x1 = static_cast<std::uint32_t>(v[1]);
-        *reinterpret_cast<std::uint16_t*>(row + j) = static_cast<std::uint16_t>((x0 >> 8) | (x1 & 0xFF00u));
+        *reinterpret_cast<std::uint16_t*>(row + j) =
+            static_cast<std::uint16_t>(__byte_perm(v[0], v[1], 0x2251));
         *reinterpret_cast<std::uint16_t*>(row + c + j) =
-            static_cast<std::uint16_t>((x0 & 255u) | ((x1 & 255u) << 8));
+            static_cast<std::uint16_t>(__byte_perm(v[0], v[1], 0x2240));
     };
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         put(PL_S1 + k, s[k]);
         put(PL_T1 + k, t[k]);
     }
-    put(PL_A11, a11);
-    put(PL_A12, a12);
-    put(PL_A22, a22);
-    put(PL_B11, b11);
-    put(PL_B21, b21);
-    put(PL_B22, b22);
+    put(PL_A11, a[0]);
+    put(PL_A12, a[1]);
+    put(PL_A22, a[3]);
+    put(PL_B11, b[0]);
+    put(PL_B21, b[2]);
+    put(PL_B22, b[3]);
     if (P.beta != 0) {
         std::uint16_t* c11 = reinterpret_cast<std::uint16_t*>(P.C.q[0]) + 4 * (r * P.C.ld + j);
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-            reinterpret_cast<uint2*>(c11)[e] = make_uint2(
-                static_cast<std::uint32_t>(R.cin[0][e]) | (static_cast<std::uint32_t>(R.cin[1][e]) << 16),
-                static_cast<std::uint32_t>(R.cin[2][e]) | (static_cast<std::uint32_t>(R.cin[3][e]) << 16));
+            reinterpret_cast<uint2*>(c11)[e] =
+                make_uint2(d2u(R.cin[0][e]) | (d2u(R.cin[1][e]) << 16),
+                           d2u(R.cin[2][e]) | (d2u(R.cin[3][e]) << 16));
     }
 }
 
@@ -155,52 +184,50 @@ __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::
 // through L2 (written by other CTAs of the same grid).
 template <bool CG>
 __device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_t r, std::uint64_t j) {
-    const double p = P.pd, pinv = P.pinv;
-    double pv[7][2];
+    const double pd = P.pd, pinv = P.pinv;
+    const std::uint32_t p = static_cast<std::uint32_t>(pd);
+    std::uint32_t w[7];
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
         const std::uint32_t* a = reinterpret_cast<const std::uint32_t*>(P.P[k] + r * P.pld[k] + j);
-        const std::uint32_t w = CG ? __ldcg(a) : *a;
-        pv[k][0] = static_cast<double>(w & 0xFFFFu);
-        pv[k][1] = static_cast<double>(w >> 16);
+        w[k] = CG ? __ldcg(a) : *a;
     }
-    double cin[2][4];  // [col e][quadrant]
+    std::uint32_t cin[2][4];  // [col e][quadrant], beta * C_in mod p
     if (P.beta != 0 && P.cin_f64) {
         // C kept its float64 C_in (the planes live in dead blocks): this thread
         // reads exactly the positions it writes
+        double2 x[4];
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) x[qd] = *reinterpret_cast<const double2*>(P.C.q[qd] + r * P.C.ld + j);
         const double be = static_cast<double>(P.beta);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-            const double2 x = *reinterpret_cast<const double2*>(P.C.q[qd] + r * P.C.ld + j);
-            cin[0][qd] = rmod(be * x.x, p, pinv);
-            cin[1][qd] = rmod(be * x.y, p, pinv);
+            cin[0][qd] = d2u(P.beta == 1 ? x[qd].x : rmod(be * x[qd].x, pd, pinv));
+            cin[1][qd] = d2u(P.beta == 1 ? x[qd].y : rmod(be * x[qd].y, pd, pinv));
         }
     } else if (P.beta != 0) {
         const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const uint2* a = reinterpret_cast<const uint2*>(c11 + 4 * (r * P.C.ld + j + e));
-            const uint2 w = CG ? __ldcg(a) : *a;
-            cin[e][0] = static_cast<double>(w.x & 0xFFFFu);
-            cin[e][1] = static_cast<double>(w.x >> 16);
-            cin[e][2] = static_cast<double>(w.y & 0xFFFFu);
-            cin[e][3] = static_cast<double>(w.y >> 16);
-        }
+        const uint4* a = reinterpret_cast<const uint4*>(c11 + 4 * (r * P.C.ld + j));
+        const uint4 v = CG ? __ldcg(a) : *a;  // positions j and j + 1, four quadrants each
+        cin[0][0] = v.x & 0xFFFFu, cin[0][1] = v.x >> 16, cin[0][2] = v.y & 0xFFFFu, cin[0][3] = v.y >> 16;
+        cin[1][0] = v.z & 0xFFFFu, cin[1][1] = v.z >> 16, cin[1][2] = v.w & 0xFFFFu, cin[1][3] = v.w >> 16;
     }
-    const double al = static_cast<double>(P.alpha);
     double out[4][2];  // [quadrant][col]
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-        const double p1 = pv[0][e], p2 = pv[1][e], p3 = pv[2][e], p4 = pv[3][e],
-                     p5 = pv[4][e], p6 = pv[5][e], p7 = pv[6][e];
-        const double u2 = p1 + p6;
-        const double u3 = u2 + p7;
-        const double u[4] = {p1 + p2, u2 + p5 + p3, u3 + (p - p4), u3 + p5};  // < 4p
+        std::uint32_t pv[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) pv[k] = e ? w[k] >> 16 : w[k] & 0xFFFFu;
+        const std::uint32_t u2 = pv[0] + pv[5], u3 = u2 + pv[6];
+        const std::uint32_t u[4] = {pv[0] + pv[1], u2 + pv[4] + pv[2], u3 + (p - pv[3]),
+                                    u3 + pv[4]};  // < 4p
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-            double v = rmod(u[qd], p, pinv) * al;
-            if (P.beta != 0) v += cin[e][qd];
-            out[qd][e] = rmod(v, p, pinv);
+            std::uint32_t v = fold4(u[qd], p);
+            if (P.alpha != 1)  // alpha v < 2^32: exact in float64
+                v = d2u(rmod(static_cast<double>(P.alpha) * u2d(v), pd, pinv));
+            if (P.beta != 0) v = addp(v, cin[e][qd], p);
+            out[qd][e] = u2d(v);
         }
     }
 #pragma unroll
