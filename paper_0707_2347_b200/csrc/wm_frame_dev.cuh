@@ -99,40 +99,110 @@ __device__ __forceinline__ void store_operand(const FrameQuads& X, const FrameFo
 // reads everything row r needs (operands, beta*C_in); after a CTA barrier,
 // phase 2 writes the operand store-backs, the S/T and raw limb planes and the
 // packed beta*C_in -- every byte of it in row r of a host.
+//
+// Every load of phase 1 is issued before the first value is used (up to twenty
+// 16-byte loads in flight per thread): with the loads interleaved with the
+// arithmetic -- what the compiler produces under a 64-register cap -- a prep
+// with folded operands waited for memory four times in a row.  Residues live in
+// uint32 registers from there on.
 struct PrepRegs {
+    std::uint32_t av[4][2], bv[4][2], cin[4][2];
+};
+
+// the same row with the loads left where the arithmetic needs them (64 registers:
+// wide CTAs, c >= 512, where occupancy matters more than loads in flight)
+struct PrepRegsF64 {
     double av[4][2], bv[4][2], cin[4][2];
 };
+
+struct OperandRaw {
+    double2 a[4], b[4];
+};
+
+__device__ __forceinline__ std::uint32_t negp(std::uint32_t a, std::uint32_t p) { return a ? p - a : 0u; }
+
+__device__ __forceinline__ void operand_fetch(const FrameQuads& X, const FrameFold& F,
+                                              std::uint64_t r, std::uint64_t j, OperandRaw& w) {
+    const bool two = F.on && F.s1[0] != nullptr;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double* s0 = F.on ? F.s0[k] + r * F.ld0 : X.q[k] + r * X.ld;
+        w.a[k] = *reinterpret_cast<const double2*>(s0 + j);
+        if (two) w.b[k] = *reinterpret_cast<const double2*>(F.s1[k] + r * F.ld1 + j);
+    }
+}
+
+// The operand as integers: loaded, or folded from the parent addition's sources.
+// Signs (sa, sb in {1, p - 1}, or no second source) stay on the integer pipe;
+// general scalars take one exact float64 reduction (sa*s0 + sb*s1 < 2^33).
+__device__ __forceinline__ void operand_finish(const FrameFold& F, const OperandRaw& w, double pd,
+                                               double pinv, std::uint32_t (&v)[4][2]) {
+    const std::uint32_t p = static_cast<std::uint32_t>(pd);
+    if (!F.on) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k][0] = d2u(w.a[k].x), v[k][1] = d2u(w.a[k].y);
+        return;
+    }
+    const bool two = F.s1[0] != nullptr;
+    const bool a1 = F.sa == 1.0, am = F.sa == pd - 1.0, b1 = F.sb == 1.0, bm = F.sb == pd - 1.0;
+    if ((a1 || am) && (!two || b1 || bm)) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const std::uint32_t x = d2u(e ? w.a[k].y : w.a[k].x);
+                const std::uint32_t y = two ? d2u(e ? w.b[k].y : w.b[k].x) : 0u;
+                v[k][e] = addp(a1 ? x : negp(x, p), !two ? 0u : b1 ? y : negp(y, p), p);
+            }
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double bx = two ? w.b[k].x : 0.0, by = two ? w.b[k].y : 0.0;
+        v[k][0] = d2u(rmod(fma(F.sa, w.a[k].x, F.sb * bx), pd, pinv));
+        v[k][1] = d2u(rmod(fma(F.sa, w.a[k].y, F.sb * by), pd, pinv));
+    }
+}
+
+__device__ __forceinline__ void store_operand_u32(const FrameQuads& X, const FrameFold& F,
+                                                  std::uint64_t r, std::uint64_t j,
+                                                  const std::uint32_t (&v)[4][2]) {
+    if (!F.on || !F.writeback) return;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        *reinterpret_cast<double2*>(X.q[k] + r * X.ld + j) = make_double2(u2d(v[k][0]), u2d(v[k][1]));
+}
 
 __device__ __forceinline__ void prep_limbs_load(const FramePrepParams& P, std::uint64_t r,
                                                 std::uint64_t j, PrepRegs& R) {
     const double p = P.pd, pinv = P.pinv;
-    load_operand(P.A, P.fold[0], r, j, p, pinv, R.av);
-    load_operand(P.B, P.fold[1], r, j, p, pinv, R.bv);
+    OperandRaw wa, wb;
+    double2 x[4];
+    operand_fetch(P.A, P.fold[0], r, j, wa);
+    operand_fetch(P.B, P.fold[1], r, j, wb);
+    if (P.beta != 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = *reinterpret_cast<const double2*>(P.C.q[k] + r * P.C.ld + j);
+    }
+    operand_finish(P.fold[0], wa, p, pinv, R.av);
+    operand_finish(P.fold[1], wb, p, pinv, R.bv);
     if (P.beta != 0) {
         const double be = static_cast<double>(P.beta);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double2 x = *reinterpret_cast<const double2*>(P.C.q[k] + r * P.C.ld + j);
-            R.cin[k][0] = rmod(be * x.x, p, pinv);
-            R.cin[k][1] = rmod(be * x.y, p, pinv);
+            R.cin[k][0] = d2u(P.beta == 1 ? x[k].x : rmod(be * x[k].x, p, pinv));
+            R.cin[k][1] = d2u(P.beta == 1 ? x[k].y : rmod(be * x[k].y, p, pinv));
         }
     }
 }
 
-__device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::uint64_t r,
-                                                 std::uint64_t j, const PrepRegs& R) {
-    store_operand(P.A, P.fold[0], r, j, R.av);
-    store_operand(P.B, P.fold[1], r, j, R.bv);
+// S / T and raw limb planes and the packed beta*C_in of row r, columns j, j + 1
+__device__ __forceinline__ void prep_emit(const FramePrepParams& P, std::uint64_t r, std::uint64_t j,
+                                          const std::uint32_t (&a)[4][2],
+                                          const std::uint32_t (&b)[4][2],
+                                          const std::uint32_t (&cin)[4][2]) {
+    const std::uint32_t p = static_cast<std::uint32_t>(P.pd);  // a, b: quadrants 11, 12, 21, 22
     // S / T on the integer pipe (the float64 pipe is the narrow one on this part)
-    const std::uint32_t p = static_cast<std::uint32_t>(P.pd);
-    std::uint32_t a[4][2], b[4][2];  // quadrants 11, 12, 21, 22
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            a[k][e] = d2u(R.av[k][e]);
-            b[k][e] = d2u(R.bv[k][e]);
-        }
     std::uint32_t s[4][2], t[4][2];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -173,9 +243,47 @@ __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::
 #pragma unroll
         for (int e = 0; e < 2; ++e)
             reinterpret_cast<uint2*>(c11)[e] =
-                make_uint2(d2u(R.cin[0][e]) | (d2u(R.cin[1][e]) << 16),
-                           d2u(R.cin[2][e]) | (d2u(R.cin[3][e]) << 16));
+                make_uint2(cin[0][e] | (cin[1][e] << 16), cin[2][e] | (cin[3][e] << 16));
     }
+}
+
+__device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::uint64_t r,
+                                                 std::uint64_t j, const PrepRegs& R) {
+    store_operand_u32(P.A, P.fold[0], r, j, R.av);
+    store_operand_u32(P.B, P.fold[1], r, j, R.bv);
+    prep_emit(P, r, j, R.av, R.bv, R.cin);
+}
+
+__device__ __forceinline__ void prep_limbs_load(const FramePrepParams& P, std::uint64_t r,
+                                                std::uint64_t j, PrepRegsF64& R) {
+    const double p = P.pd, pinv = P.pinv;
+    load_operand(P.A, P.fold[0], r, j, p, pinv, R.av);
+    load_operand(P.B, P.fold[1], r, j, p, pinv, R.bv);
+    if (P.beta != 0) {
+        const double be = static_cast<double>(P.beta);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 x = *reinterpret_cast<const double2*>(P.C.q[k] + r * P.C.ld + j);
+            R.cin[k][0] = rmod(be * x.x, p, pinv);
+            R.cin[k][1] = rmod(be * x.y, p, pinv);
+        }
+    }
+}
+
+__device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::uint64_t r,
+                                                 std::uint64_t j, const PrepRegsF64& R) {
+    store_operand(P.A, P.fold[0], r, j, R.av);
+    store_operand(P.B, P.fold[1], r, j, R.bv);
+    std::uint32_t a[4][2], b[4][2], cin[4][2];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            a[k][e] = d2u(R.av[k][e]);
+            b[k][e] = d2u(R.bv[k][e]);
+            cin[k][e] = P.beta != 0 ? d2u(R.cin[k][e]) : 0u;
+        }
+    prep_emit(P, r, j, a, b, cin);
 }
 
 // U-chain combine of quadrant position (r, j), (r, j + 1): U1 = P1+P2,

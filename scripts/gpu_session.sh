@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "midsize or full_size_hash or golden_small" > gpurun_out/pytest_gpu_a.log 2>&1; echo pytest rc=$?; tail -5 gpurun_out/pytest_gpu_a.log
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "midsize or full_size_hash or golden_small" > gpurun_out/pytest_gpu_a.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/pytest_gpu_a.log
 for c in C1 C2 C3 C4; do
 echo "== $c"
 timeout 600 python bench.py --config $c --steps 20 --warmup 5 2> gpurun_out/bench_err.log | python -c "
