@@ -288,6 +288,7 @@ __device__ __forceinline__ void direct_tile(const GemmParams& P, const TmaMaps& 
         const std::uint32_t lane_off = static_cast<std::uint32_t>(lg * 32) << 16;
         std::uint16_t* crow = static_cast<std::uint16_t*>(const_cast<void*>(Cd.p)) +
                               static_cast<std::uint64_t>(i0 + row) * Cd.ld + j0 + half * (BN / 2);
+        const bool wide = (reinterpret_cast<std::uintptr_t>(Cd.p) & 31u) == 0 && Cd.ld % 16 == 0;
 #pragma unroll
         for (int q = 0; q < BN / 32; ++q) {
             std::uint32_t out[16];
@@ -296,8 +297,18 @@ __device__ __forceinline__ void direct_tile(const GemmParams& P, const TmaMaps& 
             std::uint32_t w[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) w[e] = out[2 * e] | (out[2 * e + 1] << 16);
-            reinterpret_cast<uint4*>(crow + q * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-            reinterpret_cast<uint4*>(crow + q * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            if (wide) {
+                // the thread's sixteen residues are one 32-byte sector: one 256-bit store
+                // (two 16-byte stores to different rows per warp instruction wrote every
+                // sector twice: ncu's 50% excessive store sectors)
+                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};\n" ::"l"(crow + q * 16),
+                             "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]),
+                             "r"(w[6]), "r"(w[7])
+                             : "memory");
+            } else {
+                reinterpret_cast<uint4*>(crow + q * 16)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                reinterpret_cast<uint4*>(crow + q * 16)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
         }
         if (tid == 64) WM_DSTAMP(6);
     }
