@@ -66,13 +66,6 @@ struct DSmem {
     std::uint32_t tmem_base;
 };
 
-__device__ __forceinline__ double reduce_modp(double v, double p, double pinv) {
-    const double q = floor(v * pinv);
-    double r = fma(-q, p, v);
-    r = r < 0.0 ? r + p : r;
-    return r >= p ? r - p : r;
-}
-
 // swizzled shared-memory descriptor: start, LBO, SBO (bytes), layout type
 __device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr, std::uint32_t lbo,
                                                std::uint32_t sbo, std::uint64_t layout) {
@@ -107,12 +100,6 @@ __device__ __forceinline__ std::uint32_t boff(std::uint32_t k, std::uint32_t n) 
     constexpr std::uint32_t mask = BN == 32 ? 1u : BN == 64 ? 3u : 7u;
     constexpr std::uint32_t sh = BN == 32 ? 2u : BN == 64 ? 1u : 0u;
     return k * BN + ((((n >> 4) ^ (k >> sh)) & mask) << 4) + (n & 15u);
-}
-
-// exact uint32 -> float64 without a conversion instruction: 2^52 + u has u in
-// its low mantissa word
-__device__ __forceinline__ double u2d(std::uint32_t u) {
-    return __hiloint2double(0x43300000, static_cast<int>(u)) - 4503599627370496.0;
 }
 
 // 16 accumulator columns of one TMEM lane: D_h = A_h [B_h | B_l] at [0, 2BN),
