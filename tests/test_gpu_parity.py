@@ -221,6 +221,46 @@ def test_config_full_size_hash(W, name, fused):
     ctx.set_option("direct_frames", 1)
 
 
+@pytest.mark.parametrize("layout", ["odd-ld", "base+8B", "aligned"])
+@pytest.mark.parametrize("v", ["std2", "acc2", "ip"])
+def test_unaligned_operands_fall_back(W, O, v, layout):
+    """Caller views the 16-byte vector kernels cannot take -- an odd leading
+    dimension, a base pointer 8 bytes past a 16-byte boundary -- must run on the
+    scalar / unfused paths and still be bit-exact (Matrix.wrap accepts any row
+    stride; executor.hpp:28-63 places no alignment demand on MatViews)."""
+    import torch
+    n, cutoff = 512, 128
+
+    def view():
+        if layout == "odd-ld":
+            return torch.zeros(n, n + 1, dtype=torch.float64, device="cuda")[:, :n]
+        if layout == "base+8B":
+            return torch.zeros(n, n + 2, dtype=torch.float64, device="cuda")[:, 1:n + 1]
+        return torch.zeros(n, n, dtype=torch.float64, device="cuda")
+
+    A, B, C = (W.Matrix.wrap(view()) for _ in range(3))
+    if layout == "odd-ld":
+        assert A.ld() == n + 1
+    if layout == "base+8B":
+        assert A.t.data_ptr() % 16 == 8
+    A.fill_random(31)
+    B.fill_random(32)
+    acc = _acc(v)
+    if acc:
+        C.fill_random(33)
+    a0, b0, c0 = A.to_u32(), B.to_u32(), C.to_u32()
+    rep = W.run_variant(v, A, B, C, alpha=1, beta=1 if acc else 0, cutoff=cutoff)
+    want = O.classical_modp(a0, b0, c0 if acc else None, 1, 1 if acc else 0)
+    assert (C.to_u32() == want).all(), (v, layout)
+    if layout != "aligned":
+        assert rep.fused_frames == 0, "fused frames need 16-byte aligned rows"
+    keep_a, keep_b = _contract_keeps(v)
+    if keep_a:
+        assert (A.to_u32() == a0).all()
+    if keep_b:
+        assert (B.to_u32() == b0).all()
+
+
 @pytest.mark.parametrize("c", [128, 256, 512])
 @pytest.mark.parametrize("bn", [32, 64, 128, 1032])
 @pytest.mark.parametrize("bconv", [0, 1], ids=["planes", "f64-B"])
