@@ -83,6 +83,19 @@ def main():
     for nl in (2, 3, 4, 6):
         out["model_earliest_%d_lanes" % nl] = simulate(dur, deps, None, nl=nl, policy="earliest")
     out["model_unlimited_lanes"] = simulate(dur, deps, None, policy="inf")
+    # what would shorten the step: each kind 10% faster, and cheaper edges
+    kinds = ["ADD", "MUL", "FRAME", "GROUP", "PREP", "GEMM", "COMB", "UPLOAD", "DOWNLOAD"]
+    kd = kind[:n_].tolist()
+    out["what_if_traced_lanes"] = {}
+    for kk in sorted(set(kd)):
+        d2 = [x * 0.9 if kd[i] == kk else x for i, x in enumerate(dur)]
+        out["what_if_traced_lanes"][kinds[kk] + "_10pct_faster"] = simulate(
+            d2, deps, lane[:n_].tolist(), policy="trace")
+    out["what_if_traced_lanes"]["edges_0.3us_cheaper"] = simulate(
+        dur, deps, lane[:n_].tolist(), g_same=0.7, g_cross=1.0, policy="trace")
+    if os.environ.get("WM_LANE_DUMP"):
+        json.dump({"dur": dur, "deps": deps, "kind": kd, "lane": lane[:n_].tolist()},
+                  open(os.environ["WM_LANE_DUMP"], "w"))
     print(json.dumps(out, indent=1))
 
 
