@@ -114,6 +114,8 @@ int wm_ctx_set_stream(wm_ctx* ctx, void* stream);
  *   "dead_hosts" [1]    frame planes in dead blocks (plan liveness)
  *   "cin_direct" [1]    accumulating frames: all planes outside C, C_in read by the combine
  *   "wide_plain" [1]    plain frames' GEMM at BN = 64 (c >= 256)
+ *   "early_loads" [1]   frame prep / combine read the blocks their lane predecessor does not
+ *                       write before griddepcontrol.wait (under its tail and the launch gap)
  *   "micro" [1]         plans of tiny operations as one launch (shared-memory working set)
  *   "arena_words"       (read-only) words of the context's temporary arena = the largest
  *                       schedule peak run so far (one arena shared by every plan)

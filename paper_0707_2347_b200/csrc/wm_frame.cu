@@ -128,17 +128,37 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
 // 64-register form, whose loads sit next to their arithmetic -- at c = 512 the
 // grid is 3.5 CTAs of 256 threads per SM and occupancy wins (measured on config
 // 4: 19.1 ms of prep against 22.1-24.1 ms for the hoisted form at 64-100 registers).
-template <int MAXT, bool HOIST>
+// EARLY: nothing this prep reads is written by a launch it directly depends on
+// (FramePrepParams::early): the loads go out before griddepcontrol.wait.
+template <int MAXT, bool HOIST, bool EARLY>
 __global__ void __launch_bounds__(MAXT) k_frame_prep_limbs(const FramePrepParams P) {
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    WM_PDL_EARLY_M();
-    WM_TL_BEGIN(P.tl);
+    if (!EARLY) {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        WM_PDL_EARLY_M();
+        WM_TL_BEGIN(P.tl);
+    }
     // blockDim = rows * c/2: each CTA owns whole rows (reads precede writes per row)
     const std::uint32_t half = P.c / 2;
     const std::uint64_t r = blockIdx.x * (blockDim.x / half) + threadIdx.x / half;
     const std::uint64_t j = 2 * (threadIdx.x % half);
     typename std::conditional<HOIST, fdev::PrepRegs, fdev::PrepRegsF64>::type R;
-    fdev::prep_limbs_load(P, r, j, R);
+    if constexpr (HOIST) {
+        fdev::PrepRaw W;
+        fdev::prep_limbs_fetch(P, r, j, W);
+        if (EARLY) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            WM_PDL_EARLY_M();
+            WM_TL_BEGIN(P.tl);
+        }
+        fdev::prep_limbs_finish(P, W, R);
+    } else {
+        fdev::prep_limbs_load(P, r, j, R);
+        if (EARLY) {
+            asm volatile("griddepcontrol.wait;\n" ::: "memory");
+            WM_PDL_EARLY_M();
+            WM_TL_BEGIN(P.tl);
+        }
+    }
     __syncthreads();  // row r of every host has been read before any of it is overwritten
     fdev::prep_limbs_store(P, r, j, R);
     WM_TL_END(P.tl);
@@ -146,16 +166,27 @@ __global__ void __launch_bounds__(MAXT) k_frame_prep_limbs(const FramePrepParams
 }
 
 // thread (r, 2 consecutive columns j, j+1) of the quadrant
+// EARLY: C_in is not written by a launch this one directly depends on
+// (FrameCombParams::early): it is read before griddepcontrol.wait.
+template <bool EARLY>
 __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    WM_PDL_EARLY_M();
-    WM_TL_BEGIN(P.tl);
+    if (!EARLY) {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        WM_PDL_EARLY_M();
+        WM_TL_BEGIN(P.tl);
+    }
     const std::uint32_t c2 = P.c / 2;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx < static_cast<std::uint64_t>(P.c) * c2) {
-        const std::uint64_t r = idx / c2, j = 2 * (idx - r * c2);
-        fdev::comb_pair<false>(P, r, j);
+    const bool live = idx < static_cast<std::uint64_t>(P.c) * c2;
+    const std::uint64_t r = live ? idx / c2 : 0, j = live ? 2 * (idx - r * c2) : 0;
+    fdev::CombCin cin;
+    if (live) fdev::comb_cin_fetch<false>(P, r, j, cin);
+    if (EARLY) {
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        WM_PDL_EARLY_M();
+        WM_TL_BEGIN(P.tl);
     }
+    if (live) fdev::comb_pair<false>(P, r, j, cin);
     WM_TL_END(P.tl);
     WM_PDL_LATE_M();
 }
@@ -182,18 +213,20 @@ cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s) {
         if (P.c > 2048) return cudaErrorInvalidValue;
         const unsigned rows = static_cast<unsigned>(g_prep_rows > 0 && P.c / 2 * g_prep_rows <= 1024
                                                          ? g_prep_rows : 1);
+        const std::uint64_t n = static_cast<std::uint64_t>(P.c) * (P.c / 2);
         if (rows * (P.c / 2) <= 128)
-            return launch_pdl(k_frame_prep_limbs<256, true>, P,
-                              static_cast<std::uint64_t>(P.c) * (P.c / 2), s, rows * (P.c / 2));
-        return launch_pdl(k_frame_prep_limbs<1024, false>, P,
-                          static_cast<std::uint64_t>(P.c) * (P.c / 2), s, rows * (P.c / 2));
+            return P.early ? launch_pdl(k_frame_prep_limbs<256, true, true>, P, n, s, rows * (P.c / 2))
+                           : launch_pdl(k_frame_prep_limbs<256, true, false>, P, n, s, rows * (P.c / 2));
+        return P.early ? launch_pdl(k_frame_prep_limbs<1024, false, true>, P, n, s, rows * (P.c / 2))
+                       : launch_pdl(k_frame_prep_limbs<1024, false, false>, P, n, s, rows * (P.c / 2));
     }
     return launch_pdl(k_frame_prep, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s);
 }
 
 cudaError_t launch_frame_comb(const FrameCombParams& P, cudaStream_t s) {
-    return launch_pdl(k_frame_comb, P, static_cast<std::uint64_t>(P.c) * (P.c / 2), s,
-                      g_comb_block);
+    const std::uint64_t n = static_cast<std::uint64_t>(P.c) * (P.c / 2);
+    return P.early ? launch_pdl(k_frame_comb<true>, P, n, s, g_comb_block)
+                   : launch_pdl(k_frame_comb<false>, P, n, s, g_comb_block);
 }
 
 bool frame_kernel_available() { return true; }

@@ -41,6 +41,10 @@ struct FramePrepParams {
     std::uint32_t beta;              // accumulate: pack beta*C_in into C11 slots
     double pd, pinv;
     unsigned long long* tl;          // measurement timeline slot (nullptr: off)
+    // the launch this one programmatically depends on (its predecessor on the
+    // lane) writes nothing this prep reads: the loads go out BEFORE
+    // griddepcontrol.wait, under the predecessor's tail and the launch gap
+    std::uint32_t early;
 };
 
 struct FrameCombParams {
@@ -52,6 +56,7 @@ struct FrameCombParams {
     double pd, pinv;
     unsigned long long* tl;     // measurement timeline slot (nullptr: off)
     std::uint32_t cin_f64;      // beta != 0: C_in read as float64 from C (no packing)
+    std::uint32_t early;        // C_in is not written by the lane predecessor: read it before the wait
 };
 
 cudaError_t launch_frame_prep(const FramePrepParams& P, cudaStream_t s);

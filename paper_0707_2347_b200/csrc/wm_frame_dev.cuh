@@ -173,25 +173,32 @@ __device__ __forceinline__ void store_operand_u32(const FrameQuads& X, const Fra
         *reinterpret_cast<double2*>(X.q[k] + r * X.ld + j) = make_double2(u2d(v[k][0]), u2d(v[k][1]));
 }
 
-__device__ __forceinline__ void prep_limbs_load(const FramePrepParams& P, std::uint64_t r,
-                                                std::uint64_t j, PrepRegs& R) {
-    const double p = P.pd, pinv = P.pinv;
+struct PrepRaw {
     OperandRaw wa, wb;
     double2 x[4];
-    operand_fetch(P.A, P.fold[0], r, j, wa);
-    operand_fetch(P.B, P.fold[1], r, j, wb);
+};
+
+__device__ __forceinline__ void prep_limbs_fetch(const FramePrepParams& P, std::uint64_t r,
+                                                 std::uint64_t j, PrepRaw& W) {
+    operand_fetch(P.A, P.fold[0], r, j, W.wa);
+    operand_fetch(P.B, P.fold[1], r, j, W.wb);
     if (P.beta != 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = *reinterpret_cast<const double2*>(P.C.q[k] + r * P.C.ld + j);
+        for (int k = 0; k < 4; ++k) W.x[k] = *reinterpret_cast<const double2*>(P.C.q[k] + r * P.C.ld + j);
     }
-    operand_finish(P.fold[0], wa, p, pinv, R.av);
-    operand_finish(P.fold[1], wb, p, pinv, R.bv);
+}
+
+__device__ __forceinline__ void prep_limbs_finish(const FramePrepParams& P, const PrepRaw& W,
+                                                  PrepRegs& R) {
+    const double p = P.pd, pinv = P.pinv;
+    operand_finish(P.fold[0], W.wa, p, pinv, R.av);
+    operand_finish(P.fold[1], W.wb, p, pinv, R.bv);
     if (P.beta != 0) {
         const double be = static_cast<double>(P.beta);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            R.cin[k][0] = d2u(P.beta == 1 ? x[k].x : rmod(be * x[k].x, p, pinv));
-            R.cin[k][1] = d2u(P.beta == 1 ? x[k].y : rmod(be * x[k].y, p, pinv));
+            R.cin[k][0] = d2u(P.beta == 1 ? W.x[k].x : rmod(be * W.x[k].x, p, pinv));
+            R.cin[k][1] = d2u(P.beta == 1 ? W.x[k].y : rmod(be * W.x[k].y, p, pinv));
         }
     }
 }
@@ -286,12 +293,36 @@ __device__ __forceinline__ void prep_limbs_store(const FramePrepParams& P, std::
     prep_emit(P, r, j, a, b, cin);
 }
 
+// beta * C_in of quadrant position (r, j), (r, j + 1) as fetched: float64 pairs
+// per quadrant (cin_f64) or the packed word
+struct CombCin {
+    double2 x[4];
+    uint4 packed;
+};
+
+template <bool CG>
+__device__ __forceinline__ void comb_cin_fetch(const FrameCombParams& P, std::uint64_t r,
+                                               std::uint64_t j, CombCin& c) {
+    if (P.beta == 0) return;
+    if (P.cin_f64) {
+        // C kept its float64 C_in (the planes live in dead blocks): this thread
+        // reads exactly the positions it writes
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) c.x[qd] = *reinterpret_cast<const double2*>(P.C.q[qd] + r * P.C.ld + j);
+    } else {
+        const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
+        const uint4* a = reinterpret_cast<const uint4*>(c11 + 4 * (r * P.C.ld + j));
+        c.packed = CG ? __ldcg(a) : *a;  // positions j and j + 1, four quadrants each
+    }
+}
+
 // U-chain combine of quadrant position (r, j), (r, j + 1): U1 = P1+P2,
 // U2 = P1+P6, U3 = U2+P7, U4 = U2+P5, U5 = U4+P3, U6 = U3-P4, U7 = U3+P5 and
-// C_ij = alpha*U + beta*C_in.  CG: read the product planes and the packed C_in
+// C_ij = alpha*U + beta*C_in, on the integer pipe.  CG: read the product planes
 // through L2 (written by other CTAs of the same grid).
 template <bool CG>
-__device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_t r, std::uint64_t j) {
+__device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_t r, std::uint64_t j,
+                                          const CombCin& c) {
     const double pd = P.pd, pinv = P.pinv;
     const std::uint32_t p = static_cast<std::uint32_t>(pd);
     std::uint32_t w[7];
@@ -302,21 +333,14 @@ __device__ __forceinline__ void comb_pair(const FrameCombParams& P, std::uint64_
     }
     std::uint32_t cin[2][4];  // [col e][quadrant], beta * C_in mod p
     if (P.beta != 0 && P.cin_f64) {
-        // C kept its float64 C_in (the planes live in dead blocks): this thread
-        // reads exactly the positions it writes
-        double2 x[4];
-#pragma unroll
-        for (int qd = 0; qd < 4; ++qd) x[qd] = *reinterpret_cast<const double2*>(P.C.q[qd] + r * P.C.ld + j);
         const double be = static_cast<double>(P.beta);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-            cin[0][qd] = d2u(P.beta == 1 ? x[qd].x : rmod(be * x[qd].x, pd, pinv));
-            cin[1][qd] = d2u(P.beta == 1 ? x[qd].y : rmod(be * x[qd].y, pd, pinv));
+            cin[0][qd] = d2u(P.beta == 1 ? c.x[qd].x : rmod(be * c.x[qd].x, pd, pinv));
+            cin[1][qd] = d2u(P.beta == 1 ? c.x[qd].y : rmod(be * c.x[qd].y, pd, pinv));
         }
     } else if (P.beta != 0) {
-        const std::uint16_t* c11 = reinterpret_cast<const std::uint16_t*>(P.C.q[0]);
-        const uint4* a = reinterpret_cast<const uint4*>(c11 + 4 * (r * P.C.ld + j));
-        const uint4 v = CG ? __ldcg(a) : *a;  // positions j and j + 1, four quadrants each
+        const uint4 v = c.packed;
         cin[0][0] = v.x & 0xFFFFu, cin[0][1] = v.x >> 16, cin[0][2] = v.y & 0xFFFFu, cin[0][3] = v.y >> 16;
         cin[1][0] = v.z & 0xFFFFu, cin[1][1] = v.z >> 16, cin[1][2] = v.w & 0xFFFFu, cin[1][3] = v.w >> 16;
     }

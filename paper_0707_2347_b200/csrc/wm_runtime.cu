@@ -170,6 +170,7 @@ struct CachedPlan {
     std::uint32_t micro_n = 0;
     MicroImage micro_img{};            // its shared-memory working set
     bool micro_small = false;          // every operation small: one warp walks it
+    bool early_marked = false;         // mark_early_loads has run
     ~CachedPlan() {
         if (tl) cudaFree(tl);
         if (micro) cudaFree(micro);
@@ -219,6 +220,8 @@ struct wm_ctx {
     int epoch = 512;            // launches per dependency epoch (all lanes join between epochs)
     bool wide_plain = true;     // plain frames' GEMM at BN = 64 (half the CTAs of BN = 32)
     bool cin_direct = true;     // accumulating frames: all planes in dead blocks, C_in read by the combine
+    int early_loads = 3;        // (bit 0 prep, bit 1 combine) prep / combine read what their lane predecessor does not write
+                                // before griddepcontrol.wait
     bool trace = false;         // measurement: per-launch start / end timeline (wm_diag_trace)
     const void* traced = nullptr;  // CachedPlan of the last traced run
     Lanes lanes;
@@ -1207,6 +1210,42 @@ void issue_dag(const std::vector<Step>& steps, const DagPlan& d, bool real, cuda
     join();
 }
 
+// Loads before griddepcontrol.wait.  A launch may start while the launches it
+// depends on directly are still running: its predecessor on the lane, and the
+// launches of other lanes it joins through events (under capture a kernel
+// launched with programmatic serialization gets programmatic edges from ALL of
+// them -- measured: reading a cross-lane producer's block before the wait gives
+// wrong results).  Everything those launches themselves waited for has completed
+// (every kernel triggers its dependents after its own wait).  So whatever none
+// of the direct predecessors writes may be read ahead of the wait, under their
+// tails and the launch gap: a prep's operand blocks (all or nothing per prep),
+// a combine's C_in.
+void mark_early_loads(std::vector<Step>& steps, const DagPlan* d, int on) {
+    int last[kLanes];
+    for (int l = 0; l < kLanes; ++l) last[l] = -1;
+    auto hit = [](const std::vector<View>& x, const std::vector<View>& y) {
+        for (const View& u : x)
+            for (const View& v : y)
+                if (u.phys_overlaps(v)) return true;
+        return false;
+    };
+    for (std::size_t j = 0; j < steps.size(); ++j) {
+        Step& s = steps[j];
+        const int lane = d ? d->lane[j] : 0;
+        if (s.kind == Step::FPREP || s.kind == Step::FCOMB) {
+            // what is read ahead: the prep's whole read set, the combine's C block
+            const std::vector<View>& reads = s.kind == Step::FPREP ? s.rd : s.wr;
+            bool free_of = true;
+            if (last[lane] >= 0) free_of = !hit(steps[last[lane]].wr, reads);
+            if (d)
+                for (int w : d->waits[j]) free_of = free_of && !hit(steps[w].wr, reads);
+            if (s.kind == Step::FPREP) s.fprep.early = (on & 1) && s.fprep.limbs && free_of ? 1u : 0u;
+            else s.fcomb.early = (on & 2) && free_of ? 1u : 0u;
+        }
+        last[lane] = static_cast<int>(j);
+    }
+}
+
 void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r) {
     if (!r) return;
     std::memset(r, 0, sizeof(*r));
@@ -1462,7 +1501,7 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
     key << variant << '|' << ctx->f.real << '|' << ctx->f.p << '|' << A.rows << 'x' << A.cols
         << 'x' << B.cols << '|' << A.ld << ',' << B.ld << ',' << C.ld << '|' << alpha.r << ','
         << beta.r << ',' << alpha.d << ',' << beta.d << '|' << cutoff << '|' << ctx->fuse_frames
-        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->micro << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
+        << ctx->batch_adds << ctx->leaf_kernel << ctx->subset << ctx->fuse_adds << ctx->gemm_engine << ctx->direct_frames << ctx->dag << ctx->fold << ctx->trace << ctx->stream_io << ctx->micro << ctx->dead_hosts << '.' << ctx->epoch << '.' << ctx->wide_plain << ctx->cin_direct << ctx->early_loads << '|' << A.ptr << ',' << B.ptr << ',' << C.ptr;
     if (io)
         for (int w = 0; w < 3; ++w)
             key << "|io" << w << ':' << io->h[w] << ',' << io->stage[w] << ',' << io->up[w] << io->down[w];
@@ -1529,6 +1568,11 @@ void run(wm_ctx* ctx, const std::string& variant, const wm_dmat& A, const wm_dma
             cp->steps, std::max(1, ctx->dag),
             io ? std::max(ctx->epoch, std::min<int>(4096, static_cast<int>(cp->steps.size())))
                : ctx->epoch));
+    if (!cp->exec && !cp->early_marked) {
+        // (the subset replays issue other launch sequences: no early loads there)
+        mark_early_loads(cp->steps, dag ? cp->dag.get() : nullptr, ctx->subset == 0 ? ctx->early_loads : 0);
+        cp->early_marked = true;
+    }
     if (ctx->trace) {
         // [start, end] globaltimer slots per launch, patched into the launch
         // parameters of this (trace-keyed) plan before its graph is captured
@@ -1784,6 +1828,7 @@ int wm_ctx_set_option(wm_ctx* ctx, const char* key, int64_t value) {
         else if (k == "epoch") ctx->epoch = value < 16 ? 16 : static_cast<int>(value);
         else if (k == "wide_plain") ctx->wide_plain = value != 0;
         else if (k == "cin_direct") ctx->cin_direct = value != 0;
+        else if (k == "early_loads") ctx->early_loads = static_cast<int>(value);
         else if (k == "trace") ctx->trace = value != 0;
         else if (k == "gemm_engine") ctx->gemm_engine = static_cast<int>(value);
         else fail(E_INVALID, "unknown option " + k);
@@ -1813,6 +1858,7 @@ int wm_ctx_get_option(wm_ctx* ctx, const char* key, int64_t* value) {
         else if (k == "epoch") *value = ctx->epoch;
         else if (k == "wide_plain") *value = ctx->wide_plain;
         else if (k == "cin_direct") *value = ctx->cin_direct;
+        else if (k == "early_loads") *value = ctx->early_loads;
         else if (k == "trace") *value = ctx->trace;
         else if (k == "gemm_engine") *value = ctx->gemm_engine;
         else fail(E_INVALID, "unknown option " + k);
