@@ -44,15 +44,17 @@ def golden():
 @pytest.fixture(params=[dict(), dict(graphs=0, batch_adds=0, fuse_adds=0),
                         dict(fuse_frames=0, leaf_kernel=1), dict(fuse_frames=0, leaf_kernel=0),
                         dict(gemm_engine=0), dict(direct_frames=0), dict(dag=0),
-                        dict(fold=0), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0)],
+                        dict(fold=0), dict(dead_hosts=0), dict(wide_plain=0), dict(cin_direct=0),
+                        dict(early_loads=0)],
                 ids=["default", "nograph", "unfused-i8", "unfused-dmma", "cpasync", "convert-frames",
-                     "one-stream", "no-fold", "no-dead-hosts", "narrow-plain", "packed-cin"])
+                     "one-stream", "no-fold", "no-dead-hosts", "narrow-plain", "packed-cin",
+                     "no-early-loads"])
 def options(request, W):
     ctx = W.Context.get()
     saved = {k: ctx.get_option(k) for k in ("graphs", "batch_adds", "fuse_frames",
                                               "leaf_kernel", "fuse_adds", "gemm_engine",
                                               "direct_frames", "dag", "fold", "dead_hosts",
-                                              "wide_plain", "cin_direct")}
+                                              "wide_plain", "cin_direct", "early_loads")}
     for k, v in request.param.items():
         ctx.set_option(k, v)
     yield request.param
@@ -219,6 +221,33 @@ def test_config_full_size_hash(W, name, fused):
     assert rep.peak_extra_words == e.peak_extra_words
     assert rep.peak_extra_bytes == 8 * e.peak_extra_words
     ctx.set_option("direct_frames", 1)
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+@pytest.mark.parametrize("lanes", [3, 5])
+def test_early_loads_repeatable(W, name, lanes):
+    """Loads issued before griddepcontrol.wait (prep operands, combine C_in) must
+    never see a block a directly awaited launch -- on the lane or across lanes --
+    is still writing: the full-size hash holds on every one of several replays of
+    the captured graph, at two lane counts (a wrong early read shows up as an
+    intermittent mismatch)."""
+    c = CFG[name]
+    ctx = W.Context.get()
+    saved = ctx.get_option("dag")
+    ctx.set_option("dag", lanes)
+    try:
+        A, B, C = _problem(W, c["m"], c["k"], c["n"], c["seed"], bool(c["beta"]))
+        for rep in range(4):
+            if rep:
+                if c["variant"] == "iprect":  # overwrites its inputs
+                    A.fill_random(c["seed"])
+                    B.fill_random(c["seed"] + 1)
+                if c["beta"]:
+                    C.fill_random(c["seed"] + 2)
+            W.run_variant(c["variant"], A, B, C, alpha=c["alpha"], beta=c["beta"], cutoff=c["cutoff"])
+            assert "%016x" % C.hash() == c["appendix_a"], (name, lanes, rep)
+    finally:
+        ctx.set_option("dag", saved)
 
 
 @pytest.mark.parametrize("layout", ["odd-ld", "base+8B", "aligned"])
