@@ -1244,6 +1244,14 @@ void mark_early_loads(std::vector<Step>& steps, const DagPlan* d, int on) {
         }
         last[lane] = static_cast<int>(j);
     }
+    if (std::getenv("WM_EARLY_DUMP")) {  // how many launches read ahead of their wait
+        int np = 0, ep = 0, nc = 0, ec = 0;
+        for (const Step& s : steps) {
+            np += s.kind == Step::FPREP, ep += s.kind == Step::FPREP && s.fprep.early;
+            nc += s.kind == Step::FCOMB, ec += s.kind == Step::FCOMB && s.fcomb.early;
+        }
+        std::fprintf(stderr, "early loads: %d of %d preps, %d of %d combines\n", ep, np, ec, nc);
+    }
 }
 
 void fill_report(const Plan& plan, const std::vector<Step>* steps, wm_report* r) {
