@@ -11,6 +11,13 @@ extern int g_prep_rows;
 extern unsigned g_comb_block;
 }  // namespace wm
 
+// INVARIANT (the early loads of wm_frame.cu rely on it, wm_runtime.cu
+// mark_early_loads): every kernel executes griddepcontrol.wait BEFORE it triggers
+// its dependents (WM_PDL_EARLY_* / WM_PDL_LATE_* come after the wait; a kernel
+// without a trigger releases them when it exits).  A dependent's code ahead of
+// its own wait therefore runs only after everything its direct predecessors
+// waited for has completed.
+//
 // Where a kernel lets its programmatic dependents launch.  A dependent launched
 // early parks its CTAs at griddepcontrol.wait on the SMs the running kernel
 // uses; for compute-bound kernels that costs issue slots (measured: the float64
