@@ -132,15 +132,15 @@ __global__ void __launch_bounds__(128) k_frame_prep(const FramePrepParams P) {
 // (FramePrepParams::early): the loads go out before griddepcontrol.wait.
 template <int MAXT, bool HOIST, bool EARLY>
 __global__ void __launch_bounds__(MAXT) k_frame_prep_limbs(const FramePrepParams P) {
+    // blockDim = rows * c/2: each CTA owns whole rows (reads precede writes per row)
+    const std::uint32_t half = P.c / 2;
+    const std::uint64_t r = blockIdx.x * (blockDim.x / half) + threadIdx.x / half;
+    const std::uint64_t j = 2 * (threadIdx.x % half);
     if (!EARLY) {
         asm volatile("griddepcontrol.wait;\n" ::: "memory");
         WM_PDL_EARLY_M();
         WM_TL_BEGIN(P.tl);
     }
-    // blockDim = rows * c/2: each CTA owns whole rows (reads precede writes per row)
-    const std::uint32_t half = P.c / 2;
-    const std::uint64_t r = blockIdx.x * (blockDim.x / half) + threadIdx.x / half;
-    const std::uint64_t j = 2 * (threadIdx.x % half);
     typename std::conditional<HOIST, fdev::PrepRegs, fdev::PrepRegsF64>::type R;
     if constexpr (HOIST) {
         fdev::PrepRaw W;
@@ -170,15 +170,16 @@ __global__ void __launch_bounds__(MAXT) k_frame_prep_limbs(const FramePrepParams
 // (FrameCombParams::early): it is read before griddepcontrol.wait.
 template <bool EARLY>
 __global__ void __launch_bounds__(256) k_frame_comb(const FrameCombParams P) {
+    // the position is worked out ahead of the wait in both variants
+    const std::uint32_t c2 = P.c / 2;
+    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
+    const bool live = idx < static_cast<std::uint64_t>(P.c) * c2;
+    const std::uint64_t r = live ? idx / c2 : 0, j = live ? 2 * (idx - r * c2) : 0;
     if (!EARLY) {
         asm volatile("griddepcontrol.wait;\n" ::: "memory");
         WM_PDL_EARLY_M();
         WM_TL_BEGIN(P.tl);
     }
-    const std::uint32_t c2 = P.c / 2;
-    const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    const bool live = idx < static_cast<std::uint64_t>(P.c) * c2;
-    const std::uint64_t r = live ? idx / c2 : 0, j = live ? 2 * (idx - r * c2) : 0;
     fdev::CombCin cin;
     if (live) fdev::comb_cin_fetch<false>(P, r, j, cin);
     if (EARLY) {

@@ -102,16 +102,15 @@ namespace {
 // One kernel per run (GID): each launch carries only its own body.
 template <bool REAL, int GID>
 __global__ void __launch_bounds__(256) k_group(const fused::GroupParams G, unsigned long long* tl) {
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    WM_PDL_EARLY_M();
-    WM_TL_BEGIN(tl);
+    // the position is worked out ahead of the wait (nothing here touches memory)
     const std::uint32_t cv = G.cols >> 1;
     const std::uint64_t total = static_cast<std::uint64_t>(G.rows) * cv;
     const std::uint64_t idx = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x;
-    if (idx < total) {
-        const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
-        fused::GroupBody<REAL, GID>::run(G, r, c);
-    }
+    const std::uint64_t r = idx / cv, c = (idx - r * cv) * 2;
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    WM_PDL_EARLY_M();
+    WM_TL_BEGIN(tl);
+    if (idx < total) fused::GroupBody<REAL, GID>::run(G, r, c);
     WM_TL_END(tl);
     WM_PDL_LATE_M();
 }
